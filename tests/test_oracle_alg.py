@@ -1,0 +1,166 @@
+"""Pins of the oracle iteration — CPU only.
+
+Algorithm 1 has no external value to compare with for
+M > 1 (P9 "parity unpinned"); its parts are pinned here:
+  P7a  Alg. 1 with M = 1 equals the literal Eq. 25 iteration with an explicit
+       G^{1/2}, nu stays 0, for
+       alpha in {1, 1.5, 1.999}, fixed rho and Eq. 37;
+  P7b  alpha = 1: Alg. 1 == Alg. 2 == unrelaxed OS-LALM;
+  P7c  quadratic potential, M = 1: Alg. 1 converges to the dense PWLS
+       minimiser (A'WA + H_R)^{-1}A'Wy; alpha = 1.999 gets there in fewer
+       iterations than alpha = 1 (Theorem 2);
+  P8   Eq. 37 values, subset partition, work accounting, feasibility.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import alg, dense
+from oracle import projector as P
+from synth.configs import DIRECTIONS
+from tests.geoms import tiny
+
+
+def tiny_problem(kind="fan2d_arc", potential="hyperbola", beta=None, seed=0, **over):
+    g = tiny(kind, **over)
+    rng = np.random.default_rng(seed)
+    shape = P.vol_shape(g)
+    xt = 0.02 + 0.01 * rng.random(shape)
+    ell = P.forward(g, xt)
+    I0 = 1e4
+    c = np.maximum(rng.poisson(I0 * np.exp(-ell)).astype(np.float64), 1.0)
+    y = np.log(I0 / c)
+    w = c / I0 * 10.0           # counts, rescaled to keep D_L O(1e2)
+    n_dirs = 13 if g["dim"] == 3 else 4
+    if beta is None:
+        beta = 5.0
+    betas = [beta] * n_dirs
+    prob = alg.Problem(g, y, w, potential, 0.01, betas, n_dirs)
+    x0 = np.clip(xt + 0.005 * rng.standard_normal(shape), 0, None)
+    return prob, x0, xt
+
+
+# ------------------------------------------------------------------ P8
+def test_rho_eq37_values():
+    # Direct evaluation of Eq. 37; values cross-checked
+    # with SPEC.md:298-299 (0.97227 +- 1e-4, 0.72262 +- 1e-4) — see
+    # tests/golden/rho_eq37.txt.
+    golden = {}
+    with open("tests/golden/rho_eq37.txt") as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                k, a, v = line.split()
+                golden[(int(k), float(a))] = float(v)
+    for (k, a), v in golden.items():
+        assert abs(alg.rho_k(k, a) - v) <= 1e-6, (k, a)
+    assert alg.rho_k(0, 1.999) == 1.0
+    for a in (1.0, 1.3, 1.5, 1.999):
+        seq = [alg.rho_k(k, a) for k in range(1, 3001)]
+        assert all(s > 0 for s in seq) and all(b < c for b, c in zip(seq[1:], seq[:-1]))
+
+
+def test_subsets_partition_gradient():
+    prob, x0, _ = tiny_problem("helical_arc")
+    M = 5
+    full = prob.grad_L(x0)
+    parts = sum(prob.grad_L_subset(x0, m, M) for m in range(M))
+    assert np.allclose(parts, full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+    views = sorted(v for m in range(M) for v in range(m, prob.g["na"], M))
+    assert views == list(range(prob.g["na"]))
+
+
+def test_work_accounting_and_feasibility():
+    prob, x0, _ = tiny_problem("axial_flat")
+    DL = prob.D_L()
+    M = 3
+    g, h = alg.alg1_init(prob, x0, M, DL)
+    prob.n_fwd = prob.n_back = 0
+    x, k = x0, 0
+    for _ in range(7):
+        x, g, h, k = alg.alg1_run(prob, x, g, h, k, 1, M, 1.999, DL)
+        assert x.min() >= 0.0
+    assert prob.n_fwd == 7 and prob.n_back == 7 and k == 7
+
+
+def test_zero_data_zero_init_stays_zero():
+    prob, x0, _ = tiny_problem()
+    prob.y[:] = 0.0
+    x = alg.alg1(prob, np.zeros_like(x0), 4, 1.999, 3)[0]
+    assert np.all(x == 0.0)
+
+
+# ------------------------------------------------------------------ P7a
+@pytest.mark.parametrize("alpha", [1.0, 1.5, 1.999])
+@pytest.mark.parametrize("rho_mode", ["fixed", "continuation"])
+def test_alg1_M1_equals_literal_eq25(alpha, rho_mode):
+    prob, x0, _ = tiny_problem("fan2d_arc", nx=8, ny=8, ns=16, na=12)
+    g = prob.g
+    DL = prob.D_L().ravel()
+    A = dense.dense_A(g)
+    sw = np.sqrt(prob.w.ravel())
+    Aw, yw = sw[:, None] * A, sw * prob.y.ravel()       # Eq. 36 substitution
+    n = 100
+    rhos = [0.3] * n if rho_mode == "fixed" else [alg.rho_k(k, alpha) for k in range(n)]
+
+    def psi_grad(x):
+        return prob.reg(x.reshape(P.vol_shape(g)))[0].ravel()
+
+    def psi_curv(x):
+        return prob.reg(x.reshape(P.vol_shape(g)))[1].ravel()
+
+    xs_lit, nus = dense.literal_eq25(Aw, yw, DL, x0.ravel(), alpha, rhos, psi_grad, psi_curv)
+    xs_33 = dense.eq33(Aw, yw, DL, x0.ravel(), alpha, rhos, psi_grad, psi_curv)
+    trace = {}
+    alg.alg1(prob, x0, 1, alpha, n, DL=DL.reshape(x0.shape), rho_mode="continuation" if rho_mode != "fixed"
+             else "fixed", rho_fixed=0.3, trace=trace)
+    scale = max(np.abs(xs_lit[-1]).max(), 1e-30)
+    for k in range(1, n + 1):
+        assert np.max(np.abs(trace[k][0].ravel() - xs_lit[k])) <= 1e-10 * max(1.0, scale), k
+        assert np.max(np.abs(xs_33[k] - xs_lit[k])) <= 1e-10 * max(1.0, scale), k
+        assert np.all(nus[k] == 0.0)
+    # the iteration moves (not a trivial fixed point)
+    assert np.max(np.abs(xs_lit[-1] - xs_lit[0])) > 1e-4
+
+
+# ------------------------------------------------------------------ P7b
+def test_alpha1_collapse():
+    prob, x0, _ = tiny_problem("helical_arc")
+    DL = prob.D_L()
+    M, iters = 4, 15                    # 60 sub-iterations
+    x1 = alg.alg1(prob, x0, M, 1.0, iters, DL=DL)[0]
+    x2 = alg.alg2(prob, x0, M, 1.0, iters, DL=DL)[0]
+    x3 = alg.os_lalm_unrelaxed(prob, x0, M, iters, DL=DL)
+    nrm = np.linalg.norm(x3)
+    assert np.linalg.norm(x1 - x3) <= 1e-12 * nrm
+    assert np.linalg.norm(x2 - x3) <= 1e-12 * nrm
+    # and relaxation really changes the iterates
+    xr = alg.alg1(prob, x0, M, 1.999, iters, DL=DL)[0]
+    assert np.linalg.norm(xr - x3) > 1e-6 * nrm
+
+
+# ------------------------------------------------------------------ P7c
+def test_converges_to_dense_pwls_minimiser():
+    prob, x0, xt = tiny_problem("fan2d_arc", potential="quadratic", beta=0.5, nx=8, ny=8, ns=16, na=12)
+    g = prob.g
+    A = dense.dense_A(g)
+    xhat = dense.dense_pwls_quadratic(A, prob.w.ravel(), prob.y.ravel(), P.vol_shape(g),
+                                      DIRECTIONS[:prob.n_dirs], prob.betas)
+    assert xhat.min() > 0.0          # box inactive at the minimiser
+    DL = prob.D_L()
+    reach = {}
+    for alpha in (1.0, 1.999):
+        x = x0.copy()
+        gg, h = alg.alg1_init(prob, x, 1, DL)
+        k = 0
+        for it in range(20000):
+            xn, gg, h, k = alg.alg1_run(prob, x, gg, h, k, 1, 1, alpha, DL, rho_mode="fixed", rho_fixed=0.5)
+            err = np.linalg.norm(xn.ravel() - xhat) / np.linalg.norm(xhat)
+            if alpha not in reach and err < 1e-6:
+                reach[alpha] = it
+            done = np.linalg.norm(xn - x) < 1e-13 * np.linalg.norm(x)
+            x = xn
+            if done:
+                break
+        assert np.linalg.norm(x.ravel() - xhat) <= 1e-8 * np.linalg.norm(xhat), alpha
+    assert reach[1.999] < reach[1.0], reach

@@ -1,0 +1,131 @@
+"""Pins of the oracle regulariser (Eq. 35) — CPU."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+from oracle import projector as P
+from synth.configs import DIRECTIONS, _geom
+
+POTS = ["hyperbola", "fair", "quadratic"]
+
+
+def vol(nx, ny, nz, dz=1.0):
+    return _geom(dim=3 if nz > 1 else 2, nx=nx, ny=ny, nz=nz, dz=dz)
+
+
+def test_direction_table_matches_inputs_and_covers_26_neighbours():
+    assert P.directions() == DIRECTIONS
+    all_offsets = set()
+    for d in DIRECTIONS:
+        for sgn in (1, -1):
+            all_offsets.add(tuple(sgn * c for c in d))
+    expect = {o for o in itertools.product((-1, 0, 1), repeat=3) if o != (0, 0, 0)}
+    assert all_offsets == expect and len(DIRECTIONS) == 13
+    assert all(d[2] == 0 for d in DIRECTIONS[:4])
+
+
+@pytest.mark.parametrize("pot", POTS)
+def test_gradient_is_finite_difference_of_R(pot):
+    g = vol(5, 4, 3)
+    rng = np.random.default_rng(10)
+    x = rng.random((3, 4, 5)) * 0.5
+    kap = rng.uniform(0.5, 1.5, x.shape)
+    betas = rng.uniform(0.5, 2.0, 13)
+    delta = 0.3
+    _, gr, _ = P.reg(g, pot, delta, betas, 13, x, kap)
+    h = 1e-6
+    fd = np.zeros_like(x)
+    for idx in np.ndindex(x.shape):
+        xp, xm = x.copy(), x.copy()
+        xp[idx] += h
+        xm[idx] -= h
+        fd[idx] = (P.reg(g, pot, delta, betas, 13, xp, kap)[0] - P.reg(g, pot, delta, betas, 13, xm, kap)[0]) / (2 * h)
+    assert np.max(np.abs(fd - gr)) <= 1e-6 * np.max(np.abs(gr))
+
+
+@pytest.mark.parametrize("pot", POTS)
+def test_huber_sqs_majorizes_R(pot):
+    g = vol(5, 4, 3)
+    rng = np.random.default_rng(11)
+    x = rng.random((3, 4, 5))
+    kap = rng.uniform(0.5, 1.5, x.shape)
+    betas = rng.uniform(0.5, 2.0, 13)
+    delta = 0.2
+    R0, gr, cv = P.reg(g, pot, delta, betas, 13, x, kap)
+    for scale in (1e-3, 0.1, 1.0, 5.0):
+        for _ in range(25):
+            z = x + scale * rng.standard_normal(x.shape)
+            Rz = P.reg(g, pot, delta, betas, 13, z, kap)[0]
+            Q = R0 + np.sum(gr * (z - x)) + 0.5 * np.sum(cv * (z - x) ** 2)
+            assert Rz <= Q + 1e-12 * max(1.0, abs(Q))
+
+
+@pytest.mark.parametrize("pot", POTS)
+def test_constant_image_is_flat(pot):
+    g = vol(4, 5, 3)
+    x = np.full((3, 5, 4), 0.7)
+    R, gr, _ = P.reg(g, pot, 0.1, np.ones(13), 13, x)
+    assert R == 0.0 and np.all(gr == 0.0)
+
+
+@pytest.mark.parametrize("pot", POTS)
+def test_two_voxel_hand_expansion(pot):
+    # 2x1 image (a, b), one direction (1,0,0), beta = 1.7, kappa = 1:
+    # R = beta*phi(a-b), grad = beta*(phi'(a-b), -phi'(a-b)),
+    # D_R = 2*beta*omega(a-b) on both voxels.
+    g = vol(2, 1, 1)
+    a, b, beta, d = 0.9, 0.25, 1.7, 0.4
+    x = np.array([[[a, b]]])
+    R, gr, cv = P.reg(g, pot, d, [beta], 1, x)
+    t = a - b
+    if pot == "quadratic":
+        phi, dphi, om = t * t / 2, t, 1.0
+    elif pot == "hyperbola":
+        q = math.sqrt(1 + (t / d) ** 2)
+        phi, dphi, om = d * d * (q - 1), t / q, 1 / q
+    else:
+        phi, dphi, om = d * d * (abs(t) / d - math.log(1 + abs(t) / d)), t / (1 + abs(t) / d), 1 / (1 + abs(t) / d)
+    assert np.isclose(R, beta * phi, rtol=1e-14)
+    assert np.allclose(gr.ravel(), [beta * dphi, -beta * dphi], rtol=1e-14)
+    assert np.allclose(cv.ravel(), [2 * beta * om] * 2, rtol=1e-14)
+
+
+def test_hyperbola_and_fair_at_delta():
+    # hyperbola: phi'(delta) = delta/sqrt(2), omega(delta) = 1/sqrt(2);
+    # Fair: phi'(delta) = delta/2 (e.g. t = delta = 10 -> 5), omega = 1/2.
+    g = vol(2, 1, 1)
+    for pot, dp, om in [("hyperbola", 1 / math.sqrt(2), 1 / math.sqrt(2)), ("fair", 0.5, 0.5)]:
+        d = 10.0
+        _, gr, cv = P.reg(g, pot, d, [1.0], 1, np.array([[[d, 0.0]]]))
+        assert np.isclose(gr.ravel()[0], d * dp, rtol=1e-14)
+        assert np.isclose(cv.ravel()[0], 2 * om, rtol=1e-14)
+
+
+def test_chain_max_curvature_is_2_4_2():
+    # quadratic potential (omega = 1): 1-D chain of 3, beta = 1 -> D_R = (2, 4, 2).
+    g = vol(3, 1, 1)
+    _, _, cv = P.reg(g, "quadratic", 1.0, [1.0], 1, np.random.default_rng(0).random((1, 1, 3)))
+    assert np.allclose(cv.ravel(), [2.0, 4.0, 2.0])
+
+
+def test_borders_drop_out_of_volume_pairs():
+    # quadratic potential, unit betas: D_R = 2 * (number of in-volume neighbours).
+    g = vol(3, 3, 3)
+    _, _, cv = P.reg(g, "quadratic", 1.0, np.ones(13), 13, np.zeros((3, 3, 3)))
+    assert cv[1, 1, 1] == 2 * 26 and cv[0, 0, 0] == 2 * 7 and cv[0, 1, 1] == 2 * 17
+    g2 = vol(4, 4, 1)
+    _, _, cv2 = P.reg(g2, "quadratic", 1.0, np.ones(4), 4, np.zeros((1, 4, 4)))
+    assert cv2[0, 1, 1] == 2 * 8 and cv2[0, 0, 0] == 2 * 3
+
+
+def test_sampled_reg_matches_full():
+    g = vol(6, 5, 4)
+    rng = np.random.default_rng(12)
+    x = rng.random((4, 5, 6))
+    kap = rng.uniform(0.5, 1.5, x.shape)
+    _, gr, cv = P.reg(g, "hyperbola", 0.05, np.arange(1, 14) / 7.0, 13, x, kap)
+    idx = rng.integers(0, x.size, 40)
+    g2, c2 = P.reg_at(g, "hyperbola", 0.05, np.arange(1, 14) / 7.0, 13, x, idx, kap)
+    assert np.allclose(g2, gr.ravel()[idx], rtol=1e-15) and np.allclose(c2, cv.ravel()[idx], rtol=1e-15)
