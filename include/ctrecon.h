@@ -1,0 +1,221 @@
+/*
+ * ctrecon.h — C-ABI of the B200-native relaxed OS-LALM hot path
+ * (Nien & Fessler, "Relaxed Linearized Algorithms for Faster X-Ray CT Image
+ * Reconstruction", arXiv 1512.04564; the text is PAPER.md, cited as P:line).
+ *
+ * Library: paper_1512_04564_b200/libctrecon.so (sm_100a).  Every function is
+ * extern "C", returns ct_status (or void), never throws, and validates all
+ * arguments BEFORE launching anything: a call that returns an error has no
+ * side effects.  ct_last_error() gives a thread-local message.
+ *
+ * Memory: every float* / int64_t* array argument is a DEVICE pointer owned by
+ * the caller unless stated otherwise.  The library allocates device memory
+ * only for the small per-view table inside ct_geom and for the NCCL
+ * communicator inside ct_dist; the solver's scratch is a caller-provided
+ * workspace sized by oslalm_workspace_size().  All work is asynchronous on
+ * the given stream; asynchronous CUDA faults surface as CT_E_CUDA from the
+ * next call or from ct_sync().
+ *
+ * Layouts (C order, last index fastest):
+ *   volume      float[nz][ny][nx]          (2-D: nz = 1)
+ *   projections float[views][nt][ns]       (2-D: nt = 1), view index first
+ *   full sinogram arrays (y, w) hold all na views; a view descriptor selects
+ *   rows of them.
+ */
+#ifndef CTRECON_H
+#define CTRECON_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ct_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    CT_OK = 0,
+    CT_E_SHAPE = 1,    /* inconsistent sizes / view index out of range          */
+    CT_E_CONFIG = 2,   /* bad parameter: alpha, rho, M, delta, box, geometry      */
+    CT_E_NUMERIC = 3,  /* non-finite iterate detected                             */
+    CT_E_DIVERGED = 4, /* reserved (cost guard)                                   */
+    CT_E_CUDA = 5,     /* CUDA runtime / launch fault                             */
+    CT_E_NCCL = 6,     /* NCCL fault                                              */
+    CT_E_NOMEM = 7     /* workspace too small                                     */
+} ct_status;
+
+typedef enum { CT_DET_FLAT = 0, CT_DET_ARC = 1 } ct_det_shape;
+
+/*
+ * Scanner geometry ("A is the forward projection matrix of a CT
+ * scan"; the paper cites a separable-footprint projector [long:10:3fa] and
+ * does not define it — the projector implemented here is DESIGN.md §3 /
+ * SURVEY.md 8c.1).  Lengths in mm, angles in degrees.
+ *   voxel centre i:  (i - (nx-1)/2) dx + offset_x  (likewise y, z)
+ *   view v:          beta_v = orbit_start + orbit * v / na
+ *                    source (Dso cos beta, Dso sin beta, z_s(v)),
+ *                    z_s(v) = source_z0 + v * pitch * nt*dt*Dso/Dsd * (orbit/360) / na
+ *   column centre s: (s - (ns-1)/2 - offset_s) * Delta, Delta = ds (flat, mm at
+ *                    the detector) or ds/Dsd (arc, radians)
+ *   row centre t:    (t - (nt-1)/2 - offset_t) * dt
+ * dim = 2: fan beam, nz = nt = 1, z ignored.  dim = 3: cone beam (pitch 0 =
+ * axial, > 0 = helical).
+ */
+typedef struct {
+    int32_t dim;
+    int32_t nx, ny, nz;
+    double dx, dy, dz;
+    double offset_x, offset_y, offset_z;
+    int32_t det_shape; /* ct_det_shape */
+    int32_t ns, nt;
+    double ds, dt;
+    double offset_s, offset_t;
+    double dso, dsd;
+    int32_t na;
+    double orbit_deg, orbit_start_deg, pitch, source_z0;
+} ct_geom_desc;
+
+/* Arithmetic progression of views {start, start+stride, ...} (count terms).
+ * Subset m of M ("L_m ... the m-th subset"; reading R4):
+ * {m, M, ceil((na-m)/M)}.  Every index must be < na (else CT_E_SHAPE). */
+typedef struct {
+    int32_t start, stride, count;
+} ct_views;
+
+/* Edge-preserving regulariser of Eq. 35:
+ *   R(x) = sum_i beta_i sum_n kappa_n kappa_{n+s_i} phi([C_i x]_n)
+ * over n_dirs directions (13 in 3-D = 26 neighbours; 4 in 2-D).  The
+ * direction order is fixed (offsets in voxels):
+ *   0 (1,0,0) 1 (0,1,0) 2 (1,1,0) 3 (1,-1,0) 4 (0,0,1) 5 (1,0,1) 6 (-1,0,1)
+ *   7 (0,1,1) 8 (0,-1,1) 9 (1,1,1) 10 (-1,1,1) 11 (1,-1,1) 12 (-1,-1,1)
+ * Potentials: quadratic t^2/2; hyperbola delta^2(sqrt(1+(t/delta)^2)-1);
+ * Fair delta^2(|t/delta| - log(1+|t/delta|)).  delta > 0. */
+typedef enum { CT_POT_QUADRATIC = 0, CT_POT_HYPERBOLA = 1, CT_POT_FAIR = 2 } ct_potential;
+
+typedef struct {
+    int32_t potential; /* ct_potential */
+    double delta;
+    int32_t n_dirs;    /* 4 or 13 */
+    double beta[13];   /* beta_i >= 0 */
+} ct_reg_desc;
+
+typedef enum { OSLALM_RHO_CONTINUATION = 0, OSLALM_RHO_FIXED = 1 } oslalm_rho_mode;
+typedef enum { OSLALM_INIT_LAST_SUBSET = 0, OSLALM_INIT_FULL = 1 } oslalm_init_grad;
+
+/* Algorithm 1 inputs ("M >= 1, 1 <= alpha < 2").  box = [box_lo, box_hi]
+ * is Omega; box_hi = +inf for the non-negativity constraint. */
+typedef struct {
+    int32_t M;
+    double alpha;
+    int32_t rho_mode;  /* oslalm_rho_mode; CONTINUATION = Eq. 37 */
+    double rho_fixed;  /* used when rho_mode == FIXED, > 0 */
+    int32_t init_grad; /* oslalm_init_grad; LAST_SUBSET = P:336 literally */
+    double box_lo, box_hi;
+} oslalm_params;
+
+/*
+ * Solver state (device arrays of the volume size, caller-owned):
+ *   x       image ("x"), in/out
+ *   g       P:336-342 "g" (= A'(u - y))
+ *   htilde  D_L x - h, where h is Algorithm 1's h.  The library
+ *           carries htilde instead of h: the two are algebraically identical
+ *           updates, but htilde avoids the float32
+ *           cancellation of D_L x - h in line 4.  oslalm_state_h() recovers h.
+ *   k       number of sub-iterations done (Eq. 37 counter).  k == 0
+ *           on entry runs line 1 of Alg. 1 (rho = 1, zeta = g = M grad L_M(x),
+ *           h = D_L x - zeta) before the first sub-iteration.
+ */
+typedef struct {
+    float* x;
+    float* g;
+    float* htilde;
+    int64_t k;
+} oslalm_state;
+
+typedef struct ct_geom ct_geom; /* opaque; immutable after creation */
+typedef struct ct_dist ct_dist; /* opaque NCCL communicator wrapper  */
+
+/* Geometry handle on CUDA device `device`.  Precomputes the per-view table
+ * (cos beta, sin beta, z_s) in double, stored as float on the device.
+ * Errors: CT_E_CONFIG (non-positive sizes/spacings, dso <= 0, dsd <= 0,
+ * source inside the volume's circumscribed cylinder, footprint wider than
+ * 16 detector columns), CT_E_CUDA. */
+ct_status ct_geom_create(const ct_geom_desc* d, int device, ct_geom** out);
+void ct_geom_destroy(ct_geom* g);
+
+/* p = A x on views v (Eq. 36 is NOT applied: no weights).
+ * x: volume; proj: float[v.count][nt][ns] (overwritten). */
+ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, float* proj, ct_stream s);
+
+/* x_out (=|+=) scale * A' proj on views v.
+ * proj: float[v.count][nt][ns]; accumulate != 0 adds into x_out. */
+ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, int accumulate, float* x_out,
+                  ct_stream s);
+
+/* SQS diagonal D_L = diag(A' W A 1) over all na views.
+ * w: full sinogram weights float[na][nt][ns] (NULL = all ones); d_out: volume.
+ * workspace: device scratch of >= nt*ns*4 bytes (more = fewer chunks).
+ * dist != NULL: each rank projects its share of views and the result is
+ * summed with ncclAllReduce (identical on all ranks). */
+ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist* dist, float* d_out, void* workspace,
+                      size_t workspace_bytes, ct_stream s);
+
+/* grad = nabla R(x), curv = Huber curvature D_R(x) = 2 sum beta kappa kappa omega(x_j - x_n)
+ * (factor 2 = separable quadratic surrogate split, R6).
+ * kappa NULL = ones; curv NULL = skip. */
+ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const float* x, const float* kappa, float* grad,
+                      float* curv, ct_stream s);
+
+/* Workspace bytes needed by oslalm_relaxed_solve for this geometry/params/dist. */
+ct_status oslalm_workspace_size(const ct_geom* g, const oslalm_params* p, const ct_dist* dist, size_t* bytes);
+
+/*
+ * Run n_subiters sub-iterations of Algorithm 1 from state st:
+ *   s  = rho (D_L x - h) + (1 - rho) g
+ *   x+ = [x - (rho D_L + D_R)^{-1} (s + grad R(x))]_Omega
+ *   zeta = M grad L_m(x+),  grad L_m(x) = A_m' W_m (A_m x - y_m)   (Eq. 36)
+ *   g+ = rho/(rho+1) (alpha zeta + (1-alpha) g) + g/(rho+1)
+ *   h+ = alpha (D_L x+ - zeta) + (1 - alpha) h
+ *   rho <- rho_k(alpha) (Eq. 37), k = sub-iterations done
+ * Subset m = k mod M (views v = m mod M).  y, w: full sinograms float[na][nt][ns]
+ * (w NULL = ones).  d_l: D_L from ct_sqs_diag (required).  kappa NULL = ones.
+ * x_ref / rms_per_iter (host double[], one entry per completed outer
+ * iteration within this call) are optional; giving them synchronises.
+ * dist != NULL shards each subset's views over the ranks and sums the partial
+ * back-projections with ncclAllReduce (all ranks hold the full volume).
+ * Single-GPU calls replay a cached CUDA graph of one sub-iteration.
+ * Errors: CT_E_CONFIG (alpha not in [1,2), rho_fixed <= 0, M < 1 or M > na,
+ * box_lo > box_hi, bad regulariser), CT_E_NOMEM (workspace), CT_E_NUMERIC
+ * (non-finite x after the call), CT_E_CUDA, CT_E_NCCL.
+ */
+ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                               const float* kappa, const float* d_l, const oslalm_params* p, oslalm_state* st,
+                               int n_subiters, const float* x_ref, double* rms_per_iter, const ct_dist* dist,
+                               void* workspace, size_t workspace_bytes, ct_stream s);
+
+/* h = D_L x - htilde (Algorithm 1's h, for checkpoints and parity checks). */
+ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out, ct_stream s);
+
+/* Eq. 37, pure host function: 1 if k == 0 else
+ * pi/(alpha(k+1)) sqrt(1 - (pi/(2 alpha (k+1)))^2). */
+double oslalm_rho(int64_t k, double alpha);
+
+/* Synchronise the stream and report deferred asynchronous errors. */
+ct_status ct_sync(ct_stream s);
+
+/* NCCL plumbing (one process per GPU).  The unique id (128 bytes) is created
+ * on rank 0 and broadcast by the caller (e.g. torch.distributed). */
+ct_status ct_nccl_unique_id(unsigned char id[128]);
+ct_status ct_dist_create(int rank, int world, const unsigned char id[128], int device, ct_dist** out);
+void ct_dist_destroy(ct_dist* d);
+
+/* Number of this library's kernel launches since load (for bench accounting). */
+int64_t ct_launch_count(void);
+
+const char* ct_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTRECON_H */

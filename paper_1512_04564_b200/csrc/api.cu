@@ -1,0 +1,559 @@
+// api.cu — the extern "C" boundary of libctrecon.so (include/ctrecon.h):
+// argument validation (before any launch), geometry handle, projector /
+// regulariser entry points, the Algorithm 1 solver with its CUDA-graph replay
+// and the NCCL view-sharded path.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ctrecon.h"
+#include "kernels.cuh"
+
+using namespace ctr;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+namespace ctr {
+int64_t launches_add(int64_t n) { return g_launches.fetch_add(n) + n; }
+}  // namespace ctr
+
+static ct_status fail(ct_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CT_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return fail(CT_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CT_NCCL(call)                                                                        \
+    do {                                                                                     \
+        ncclResult_t r_ = (call);                                                            \
+        if (r_ != ncclSuccess) return fail(CT_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+    } while (0)
+
+// ------------------------------------------------------------------ handles
+struct GraphKey {
+    std::vector<uintptr_t> ptrs;
+    std::vector<double> vals;
+    bool operator<(const GraphKey& o) const { return std::tie(ptrs, vals) < std::tie(o.ptrs, o.vals); }
+};
+
+struct ct_geom {
+    ct_geom_desc d;
+    DGeom G;
+    int device;
+    float4* vtab;             // per view: cos beta, sin beta, z_s, 0
+    cudaStream_t cap_stream;  // private stream for graph capture
+    std::mutex mu;            // guards the graph cache (the geometry itself is immutable)
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+};
+
+struct ct_dist {
+    ncclComm_t comm;
+    int rank, world, device;
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+static ct_status check_async() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(CT_E_CUDA, "CUDA launch/async error: %s", cudaGetErrorString(e));
+    return CT_OK;
+}
+
+// ------------------------------------------------------------------ geometry
+static ct_status validate_desc(const ct_geom_desc* d) {
+    if (!d) return fail(CT_E_CONFIG, "ct_geom_desc is NULL");
+    if (d->dim != 2 && d->dim != 3) return fail(CT_E_CONFIG, "dim must be 2 or 3 (got %d)", d->dim);
+    if (d->nx <= 0 || d->ny <= 0 || d->nz <= 0 || d->ns <= 0 || d->nt <= 0 || d->na <= 0)
+        return fail(CT_E_CONFIG, "sizes must be positive");
+    if (d->dim == 2 && (d->nz != 1 || d->nt != 1)) return fail(CT_E_CONFIG, "2-D geometry needs nz = nt = 1");
+    if (!(d->dx > 0 && d->dy > 0 && d->dz > 0 && d->ds > 0 && d->dt > 0))
+        return fail(CT_E_CONFIG, "spacings must be positive");
+    if (!(d->dso > 0 && d->dsd > d->dso)) return fail(CT_E_CONFIG, "need 0 < dso < dsd");
+    if (d->det_shape != CT_DET_FLAT && d->det_shape != CT_DET_ARC) return fail(CT_E_CONFIG, "bad det_shape");
+    if (!std::isfinite(d->orbit_deg) || !std::isfinite(d->orbit_start_deg) || !std::isfinite(d->pitch) ||
+        !std::isfinite(d->source_z0))
+        return fail(CT_E_CONFIG, "non-finite orbit parameters");
+    if ((long long)d->nx * d->ny * d->nz > (1LL << 33)) return fail(CT_E_CONFIG, "volume too large");
+    // source must stay outside the volume's circumscribed cylinder
+    const double ex = 0.5 * d->nx * d->dx + std::fabs(d->offset_x);
+    const double ey = 0.5 * d->ny * d->dy + std::fabs(d->offset_y);
+    const double rmax = std::sqrt(ex * ex + ey * ey);
+    if (rmax >= 0.95 * d->dso) return fail(CT_E_CONFIG, "volume reaches the source circle");
+    // footprint width bound (columns) for the back-projector's per-thread slots
+    const double dmin = d->dso - rmax;
+    const double diag = std::sqrt(d->dx * d->dx + d->dy * d->dy);
+    double width;
+    if (d->det_shape == CT_DET_ARC) {
+        width = 2.0 * std::asin(std::min(1.0, 0.5 * diag / dmin)) / (d->ds / d->dsd);
+    } else {
+        const double th = std::asin(rmax / d->dso);
+        const double c = std::cos(th);
+        width = d->dsd * (diag / dmin) / (c * c) / d->ds;
+    }
+    if (width + 2.0 > kMaxCells)
+        return fail(CT_E_CONFIG, "voxel footprint spans up to %.1f detector columns (limit %d)", width + 2.0,
+                    kMaxCells);
+    return CT_OK;
+}
+
+static DGeom make_dgeom(const ct_geom_desc* d) {
+    DGeom G;
+    G.dim = d->dim;
+    G.nx = d->nx;
+    G.ny = d->ny;
+    G.nz = d->dim == 3 ? d->nz : 1;
+    G.ns = d->ns;
+    G.nt = d->dim == 3 ? d->nt : 1;
+    G.arc = d->det_shape == CT_DET_ARC;
+    G.na = d->na;
+    G.dx = (float)d->dx;
+    G.dy = (float)d->dy;
+    G.dz = (float)d->dz;
+    G.x0 = (float)(-0.5 * (d->nx - 1) * d->dx + d->offset_x);
+    G.y0 = (float)(-0.5 * (d->ny - 1) * d->dy + d->offset_y);
+    G.z0 = (float)(-0.5 * (G.nz - 1) * d->dz + d->offset_z);
+    const double delta = G.arc ? d->ds / d->dsd : d->ds;
+    G.delta = (float)delta;
+    G.inv_delta = (float)(1.0 / delta);
+    G.s_c0 = (float)(0.5 * (d->ns - 1) + d->offset_s);
+    G.t_c0p = (float)(0.5 * (G.nt - 1) + d->offset_t + 0.5);
+    G.dt = (float)d->dt;
+    G.inv_dt = (float)(1.0 / d->dt);
+    G.dso = (float)d->dso;
+    G.dsd = (float)d->dsd;
+    G.nxy = (long long)d->nx * d->ny;
+    G.nvox = G.nxy * G.nz;
+    return G;
+}
+
+extern "C" ct_status ct_geom_create(const ct_geom_desc* d, int device, ct_geom** out) {
+    if (!out) return fail(CT_E_CONFIG, "out is NULL");
+    *out = nullptr;
+    ct_status st = validate_desc(d);
+    if (st != CT_OK) return st;
+    int ndev = 0;
+    CT_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CT_E_CONFIG, "device %d not present (%d devices)", device, ndev);
+    DeviceGuard guard(device);
+    std::vector<float4> tab(d->na);
+    const double pi = 3.14159265358979323846;
+    const double zstep = d->pitch * d->nt * d->dt * d->dso / d->dsd * (d->orbit_deg / 360.0) / d->na;
+    for (int v = 0; v < d->na; v++) {
+        const double beta = d->orbit_start_deg * pi / 180.0 + (d->orbit_deg * pi / 180.0) * v / d->na;
+        tab[v] = make_float4((float)std::cos(beta), (float)std::sin(beta),
+                             (float)(d->dim == 3 ? d->source_z0 + v * zstep : 0.0), 0.f);
+    }
+    ct_geom* g = new ct_geom();
+    g->d = *d;
+    g->G = make_dgeom(d);
+    g->device = device;
+    g->vtab = nullptr;
+    cudaError_t e = cudaMalloc(&g->vtab, sizeof(float4) * d->na);
+    if (e == cudaSuccess) e = cudaMemcpy(g->vtab, tab.data(), sizeof(float4) * d->na, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        if (g->vtab) cudaFree(g->vtab);
+        delete g;
+        return fail(CT_E_CUDA, "ct_geom_create: %s", cudaGetErrorString(e));
+    }
+    *out = g;
+    return CT_OK;
+}
+
+extern "C" void ct_geom_destroy(ct_geom* g) {
+    if (!g) return;
+    DeviceGuard guard(g->device);
+    for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+    cudaStreamDestroy(g->cap_stream);
+    cudaFree(g->vtab);
+    delete g;
+}
+
+static ct_status check_views(const ct_geom* g, ct_views v) {
+    if (v.count < 0) return fail(CT_E_SHAPE, "view count %d < 0", v.count);
+    if (v.count == 0) return CT_OK;
+    if (v.stride < 1) return fail(CT_E_SHAPE, "view stride must be >= 1");
+    const long long last = (long long)v.start + (long long)(v.count - 1) * v.stride;
+    if (v.start < 0 || last >= g->d.na)
+        return fail(CT_E_SHAPE, "views {%d,%d,%d} outside [0, %d)", v.start, v.stride, v.count, g->d.na);
+    if (v.count > 65535) return fail(CT_E_SHAPE, "at most 65535 views per call (got %d)", v.count);
+    return CT_OK;
+}
+
+static Views to_views(ct_views v) { return Views{v.start, v.stride, v.count}; }
+
+// ------------------------------------------------------------------ projector
+extern "C" ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, float* proj, ct_stream s) {
+    if (!g || !x || !proj) return fail(CT_E_CONFIG, "ct_forward: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    DeviceGuard guard(g->device);
+    launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, x, x, nullptr, nullptr, proj, FWD_PLAIN,
+               (cudaStream_t)s);
+    return check_async();
+}
+
+extern "C" ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, int accumulate,
+                             float* x_out, ct_stream s) {
+    if (!g || !proj || !x_out) return fail(CT_E_CONFIG, "ct_back: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    DeviceGuard guard(g->device);
+    launch_back(g->G, g->vtab, nullptr, to_views(v), proj, scale, accumulate ? BK_ACCUM : BK_WRITE,
+                g->G.dim == 3, x_out, nullptr, nullptr, (cudaStream_t)s);
+    return check_async();
+}
+
+extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist* dist, float* d_out,
+                                 void* workspace, size_t workspace_bytes, ct_stream s) {
+    if (!g || !d_out || !workspace) return fail(CT_E_CONFIG, "ct_sqs_diag: NULL argument");
+    const size_t per_view = (size_t)g->G.nt * g->G.ns * sizeof(float);
+    int chunk = (int)std::min<size_t>(workspace_bytes / per_view, 65535);
+    if (chunk < 1) return fail(CT_E_NOMEM, "ct_sqs_diag: workspace %zu < %zu bytes", workspace_bytes, per_view);
+    DeviceGuard guard(g->device);
+    cudaStream_t cs = (cudaStream_t)s;
+    const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
+    CT_CUDA(cudaMemsetAsync(d_out, 0, sizeof(float) * g->G.nvox, cs));
+    // this rank's views: rank, rank + world, ...
+    const int mine = (g->d.na - rank + world - 1) / world;
+    float* r = (float*)workspace;
+    for (int c0 = 0; c0 < mine; c0 += chunk) {
+        const int cnt = std::min(chunk, mine - c0);
+        Views vv{rank + c0 * world, world, cnt};
+        launch_fwd(g->G, g->vtab, nullptr, vv, cnt, nullptr, nullptr, nullptr, w, r, FWD_ONES_W, cs);
+        launch_back(g->G, g->vtab, nullptr, vv, r, 1.0f, BK_ACCUM, false, d_out, nullptr, nullptr, cs);
+    }
+    ct_status st = check_async();
+    if (st != CT_OK) return st;
+    if (dist && dist->world > 1)
+        CT_NCCL(ncclAllReduce(d_out, d_out, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, cs));
+    return CT_OK;
+}
+
+static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp) {
+    if (!r) return fail(CT_E_CONFIG, "ct_reg_desc is NULL");
+    if (r->potential < 0 || r->potential > 2) return fail(CT_E_CONFIG, "bad potential %d", r->potential);
+    if (!(r->delta > 0)) return fail(CT_E_CONFIG, "delta must be > 0");
+    if (r->n_dirs != 4 && r->n_dirs != 13) return fail(CT_E_CONFIG, "n_dirs must be 4 or 13");
+    if (g->G.dim == 2 && r->n_dirs != 4) return fail(CT_E_CONFIG, "2-D geometry uses n_dirs = 4");
+    for (int i = 0; i < 13; i++) {
+        if (!(r->beta[i] >= 0) || !std::isfinite(r->beta[i])) return fail(CT_E_CONFIG, "beta[%d] must be >= 0", i);
+        rp.beta[i] = i < r->n_dirs ? (float)r->beta[i] : 0.f;
+    }
+    rp.delta = (float)r->delta;
+    rp.inv_delta = (float)(1.0 / r->delta);
+    rp.potential = r->potential;
+    rp.n_dirs = r->n_dirs;
+    return CT_OK;
+}
+
+extern "C" ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const float* x, const float* kappa,
+                                 float* grad, float* curv, ct_stream s) {
+    if (!g || !x || !grad) return fail(CT_E_CONFIG, "ct_reg_grad: NULL argument");
+    RegParams rp;
+    ct_status st = make_reg(g, r, rp);
+    if (st != CT_OK) return st;
+    DeviceGuard guard(g->device);
+    launch_reg(g->G, rp, x, kappa, grad, curv, (cudaStream_t)s);
+    return check_async();
+}
+
+// ------------------------------------------------------------------ solver
+struct WsLayout {
+    size_t ctl, xalt, r, zeta, flag, dsum, total;
+};
+
+static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dist* dist) {
+    const int world = dist ? dist->world : 1;
+    const long long vm = (g->d.na + p->M - 1) / p->M;
+    const long long vrank = (vm + world - 1) / world;
+    WsLayout L;
+    size_t off = 0;
+    L.ctl = off;
+    off = align_up(off + sizeof(Ctl));
+    L.xalt = off;
+    off = align_up(off + sizeof(float) * g->G.nvox);
+    L.r = off;
+    off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
+    L.zeta = off;
+    if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
+    L.flag = off;
+    off = align_up(off + sizeof(int));
+    L.dsum = off;
+    off = align_up(off + sizeof(double));
+    L.total = off;
+    return L;
+}
+
+static ct_status validate_params(const ct_geom* g, const oslalm_params* p) {
+    if (!p) return fail(CT_E_CONFIG, "oslalm_params is NULL");
+    if (p->M < 1 || p->M > g->d.na) return fail(CT_E_CONFIG, "M = %d outside [1, na = %d]", p->M, g->d.na);
+    if (!(p->alpha >= 1.0 && p->alpha < 2.0)) return fail(CT_E_CONFIG, "alpha = %g outside [1, 2) (P:334)", p->alpha);
+    if (p->rho_mode != OSLALM_RHO_CONTINUATION && p->rho_mode != OSLALM_RHO_FIXED)
+        return fail(CT_E_CONFIG, "bad rho_mode");
+    if (p->rho_mode == OSLALM_RHO_FIXED && !(p->rho_fixed > 0)) return fail(CT_E_CONFIG, "rho_fixed must be > 0");
+    if (p->init_grad != OSLALM_INIT_LAST_SUBSET && p->init_grad != OSLALM_INIT_FULL)
+        return fail(CT_E_CONFIG, "bad init_grad");
+    if (!(p->box_lo <= p->box_hi)) return fail(CT_E_CONFIG, "box_lo > box_hi");
+    return CT_OK;
+}
+
+extern "C" ct_status oslalm_workspace_size(const ct_geom* g, const oslalm_params* p, const ct_dist* dist,
+                                           size_t* bytes) {
+    if (!g || !bytes) return fail(CT_E_CONFIG, "oslalm_workspace_size: NULL argument");
+    ct_status st = validate_params(g, p);
+    if (st != CT_OK) return st;
+    *bytes = ws_layout(g, p, dist).total;
+    return CT_OK;
+}
+
+extern "C" double oslalm_rho(int64_t k, double alpha) {
+    if (k == 0) return 1.0;
+    const double pi = 3.14159265358979323846;
+    const double a = pi / (alpha * (double)(k + 1));
+    return a * std::sqrt(1.0 - 0.25 * a * a);
+}
+
+// one sub-iteration (lines 4-9 of Alg. 1) on stream s; single GPU.
+static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, float* xa, float* xb, const float* y,
+                            const float* w, const float* dl, float* gb, float* ht, const float* kappa, float* r,
+                            int max_count, float M, float lo, float hi, cudaStream_t s) {
+    launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, s);
+    launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
+    launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);
+    launch_advance(ctl, s);
+}
+
+extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                                          const float* kappa, const float* d_l, const oslalm_params* p,
+                                          oslalm_state* st, int n_subiters, const float* x_ref,
+                                          double* rms_per_iter, const ct_dist* dist, void* workspace,
+                                          size_t workspace_bytes, ct_stream stream) {
+    if (!g || !y || !d_l || !st || !workspace) return fail(CT_E_CONFIG, "oslalm_relaxed_solve: NULL argument");
+    if (!st->x || !st->g || !st->htilde) return fail(CT_E_CONFIG, "oslalm_state has NULL arrays");
+    if (st->k < 0) return fail(CT_E_CONFIG, "state k < 0");
+    if (n_subiters < 0) return fail(CT_E_CONFIG, "n_subiters < 0");
+    ct_status stt = validate_params(g, p);
+    if (stt != CT_OK) return stt;
+    RegParams rp;
+    stt = make_reg(g, r, rp);
+    if (stt != CT_OK) return stt;
+    const WsLayout L = ws_layout(g, p, dist);
+    if (workspace_bytes < L.total)
+        return fail(CT_E_NOMEM, "workspace %zu < %zu bytes (oslalm_workspace_size)", workspace_bytes, L.total);
+    if (dist && dist->device != g->device) return fail(CT_E_CONFIG, "ct_dist device != ct_geom device");
+
+    DeviceGuard guard(g->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* ws = (char*)workspace;
+    Ctl* ctl = (Ctl*)(ws + L.ctl);
+    float* xalt = (float*)(ws + L.xalt);
+    float* rbuf = (float*)(ws + L.r);
+    float* zeta = dist ? (float*)(ws + L.zeta) : nullptr;
+    int* dflag = (int*)(ws + L.flag);
+    double* dsum = (double*)(ws + L.dsum);
+    const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
+    const int M = p->M;
+    const int vm_max = (g->d.na + M - 1) / M;
+    const int max_count = (vm_max + world - 1) / world;
+    const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
+
+    Ctl h;
+    memset(&h, 0, sizeof(h));
+    h.k = st->k;
+    h.k_base = st->k;
+    h.M = M;
+    h.na = g->d.na;
+    h.rank = rank;
+    h.world = world;
+    h.rho_fixed_mode = p->rho_mode == OSLALM_RHO_FIXED;
+    h.alpha = (float)p->alpha;
+    h.rho_fixed = (float)p->rho_fixed;
+    CT_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+
+    // ---- line 1: rho = 1, zeta = g = M grad L_M(x), h = D_L x - zeta  (htilde = zeta)
+    if (st->k == 0) {
+        float* zdst = dist ? zeta : st->g;
+        if (p->init_grad == OSLALM_INIT_LAST_SUBSET) {
+            const int m = M - 1;
+            const int vm = (g->d.na - m + M - 1) / M;
+            const int cnt = (vm - rank + world - 1) / world;
+            Views vv{m + rank * M, world * M, cnt};
+            if (cnt > 0) {
+                launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
+                launch_back(g->G, g->vtab, nullptr, vv, rbuf, (float)M, BK_WRITE, false, zdst, nullptr, nullptr, s);
+            } else {
+                CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
+            }
+        } else {
+            const int mine = (g->d.na - rank + world - 1) / world;
+            bool first = true;
+            for (int c0 = 0; c0 < mine; c0 += max_count) {
+                const int cnt = std::min(max_count, mine - c0);
+                Views vv{rank + c0 * world, world, cnt};
+                launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
+                launch_back(g->G, g->vtab, nullptr, vv, rbuf, 1.0f, first ? BK_WRITE : BK_ACCUM, false, zdst,
+                            nullptr, nullptr, s);
+                first = false;
+            }
+            if (first) CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
+        }
+        if (dist && dist->world > 1)
+            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+        launch_init_from_zeta(g->G, zdst, st->g, st->htilde, s);
+        stt = check_async();
+        if (stt != CT_OK) return stt;
+    }
+
+    // ---- sub-iterations
+    const float Mf = (float)M;
+    int done = 0;
+    int iter_out = 0;
+    long long kcur = st->k;
+    cudaGraphExec_t exec = nullptr;
+    if (!dist && n_subiters > 0) {
+        GraphKey key;
+        key.ptrs = {(uintptr_t)ctl, (uintptr_t)st->x, (uintptr_t)xalt, (uintptr_t)y, (uintptr_t)w,
+                    (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf};
+        key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi,
+                    (double)rp.potential, (double)rp.delta, (double)rp.n_dirs};
+        for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
+        std::lock_guard<std::mutex> lk(const_cast<ct_geom*>(g)->mu);
+        auto it = g->graphs.find(key);
+        if (it != g->graphs.end()) {
+            exec = it->second;
+        } else {
+            cudaStream_t cs = g->cap_stream;
+            CT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            enqueue_subiter(g, rp, ctl, st->x, xalt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count, Mf, lo,
+                            hi, cs);
+            cudaGraph_t graph;
+            cudaError_t e = cudaStreamEndCapture(cs, &graph);
+            if (e != cudaSuccess) return fail(CT_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
+            e = cudaGraphInstantiate(&exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) return fail(CT_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+            launches_add(-4);  // capture is not a launch; replays are counted below
+            const_cast<ct_geom*>(g)->graphs[key] = exec;
+        }
+    }
+    while (done < n_subiters) {
+        if (exec) {
+            CT_CUDA(cudaGraphLaunch(exec, s));
+            launches_add(4);
+        } else {
+            launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, s);
+            launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
+            launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
+            if (dist->world > 1)
+                CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+            launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
+            launch_advance(ctl, s);
+        }
+        done++;
+        kcur++;
+        if (x_ref && rms_per_iter && kcur % M == 0) {
+            const float* xc = (done & 1) ? xalt : st->x;
+            CT_CUDA(cudaMemsetAsync(dsum, 0, sizeof(double), s));
+            launch_check(g->G, xc, x_ref, dflag, dsum, s);
+            double hs = 0.0;
+            CT_CUDA(cudaMemcpyAsync(&hs, dsum, sizeof(double), cudaMemcpyDeviceToHost, s));
+            CT_CUDA(cudaStreamSynchronize(s));
+            rms_per_iter[iter_out++] = std::sqrt(hs / (double)g->G.nvox);
+        }
+    }
+    if (n_subiters & 1) CT_CUDA(cudaMemcpyAsync(st->x, xalt, sizeof(float) * g->G.nvox, cudaMemcpyDeviceToDevice, s));
+    st->k += n_subiters;
+    // finiteness of the returned image (K7)
+    CT_CUDA(cudaMemsetAsync(dflag, 0, sizeof(int), s));
+    launch_check(g->G, st->x, nullptr, dflag, nullptr, s);
+    int hflag = 0;
+    CT_CUDA(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CT_CUDA(cudaStreamSynchronize(s));
+    stt = check_async();
+    if (stt != CT_OK) return stt;
+    if (hflag) return fail(CT_E_NUMERIC, "non-finite values in x after sub-iteration %lld", (long long)st->k);
+    return CT_OK;
+}
+
+extern "C" ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out,
+                                    ct_stream s) {
+    if (!g || !d_l || !st || !st->x || !st->htilde || !h_out) return fail(CT_E_CONFIG, "oslalm_state_h: NULL argument");
+    DeviceGuard guard(g->device);
+    launch_state_h(g->G, d_l, st->x, st->htilde, h_out, (cudaStream_t)s);
+    return check_async();
+}
+
+extern "C" ct_status ct_sync(ct_stream s) {
+    CT_CUDA(cudaStreamSynchronize((cudaStream_t)s));
+    return check_async();
+}
+
+// ------------------------------------------------------------------ NCCL
+extern "C" ct_status ct_nccl_unique_id(unsigned char id[128]) {
+    if (!id) return fail(CT_E_CONFIG, "id is NULL");
+    ncclUniqueId u;
+    static_assert(sizeof(u.internal) == 128, "ncclUniqueId size");
+    CT_NCCL(ncclGetUniqueId(&u));
+    memcpy(id, u.internal, 128);
+    return CT_OK;
+}
+
+extern "C" ct_status ct_dist_create(int rank, int world, const unsigned char id[128], int device, ct_dist** out) {
+    if (!out || !id) return fail(CT_E_CONFIG, "ct_dist_create: NULL argument");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return fail(CT_E_CONFIG, "bad rank %d / world %d", rank, world);
+    DeviceGuard guard(device);
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclComm_t comm;
+    CT_NCCL(ncclCommInitRank(&comm, world, u, rank));
+    ct_dist* d = new ct_dist{comm, rank, world, device};
+    *out = d;
+    return CT_OK;
+}
+
+extern "C" void ct_dist_destroy(ct_dist* d) {
+    if (!d) return;
+    ncclCommDestroy(d->comm);
+    delete d;
+}
+
+extern "C" int64_t ct_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char* ct_last_error(void) { return g_err.c_str(); }

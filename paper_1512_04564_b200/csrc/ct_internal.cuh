@@ -1,0 +1,183 @@
+// ct_internal.cuh — device-side geometry and separable-footprint (SF) helpers
+// shared by the forward and back-projection kernels of libctrecon.so.
+//
+// The projector is the SF model of DESIGN.md §3; the paper
+// only cites it (PAPER.md:315 [long:10:3fa]).  Forward and back projection
+// call the SAME footprint function (ct_footprint) and the same trapezoid
+// antiderivative (trap_T), so the GPU A' is the transpose of the GPU A up to
+// summation order.
+//
+// float32 numerics: corner footprints are computed relative to the column
+// centre (cross/dot of the centre ray with the corner offset), so the
+// trapezoid breakpoints are formed from O(voxel) numbers instead of
+// differences of large absolute angles / detector positions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ctr {
+
+constexpr int kMaxCells = 16;     // max detector columns under one voxel footprint
+constexpr float kRampEps = 1e-6f; // ramp widths below this (in cells) take their limit
+
+struct DGeom {
+    int dim, nx, ny, nz, ns, nt, arc, na;
+    float dx, dy, dz;
+    float x0, y0, z0;     // centre of voxel (0,0,0)
+    float delta;          // column pitch: mm (flat) or rad (arc)
+    float inv_delta;
+    float s_c0;           // (ns-1)/2 + offset_s: fractional column of tau = 0
+    float t_c0p;          // (nt-1)/2 + offset_t + 1/2: row units, row t spans [t, t+1)
+    float dt, inv_dt, dso, dsd;
+    long long nxy, nvox;
+};
+
+// Solver control block in device memory (read by every kernel of a captured
+// sub-iteration; advanced by k_advance).  Views of the current subset and
+// rho are derived on the device from k, so one CUDA graph serves every
+// sub-iteration.
+struct Ctl {
+    long long k;        // sub-iterations done (Eq. 37 counter)
+    long long k_base;   // k at the start of this solve call (x buffer parity)
+    int M, na;
+    int rank, world;    // view sharding (dist), 0/1 on a single GPU
+    int rho_fixed_mode;
+    float alpha, rho_fixed;
+    int bad;            // set by kernels on footprint overflow (debug guard)
+};
+
+struct Views {          // explicit descriptor, or subset-from-Ctl when ctl != nullptr
+    int start, stride, count;
+};
+
+__device__ __forceinline__ float rho_of_k(const Ctl* c) {
+    if (c->rho_fixed_mode) return c->rho_fixed;
+    long long k = c->k;
+    if (k == 0) return 1.0f;
+    double a = 3.14159265358979323846 / ((double)c->alpha * (double)(k + 1));
+    double b = 0.5 * a;
+    return (float)(a * sqrt(1.0 - b * b));
+}
+
+// View selection: subset m = k mod M, sharded over ranks (rank p takes the
+// subset-local views p, p+G, ...).
+__device__ __forceinline__ Views select_views(const Ctl* c, Views v) {
+    if (!c) return v;
+    int m = (int)(c->k % c->M);
+    int vm = (c->na - m + c->M - 1) / c->M;
+    Views o;
+    o.start = m + c->rank * c->M;
+    o.stride = c->world * c->M;
+    o.count = (vm - c->rank + c->world - 1) / c->world;
+    if (o.count < 0) o.count = 0;
+    return o;
+}
+
+__device__ __forceinline__ void sort4(float& a, float& b, float& c, float& d) {
+    float t;
+#define CTR_CS(p, q) if (p > q) { t = p; p = q; q = t; }
+    CTR_CS(a, b) CTR_CS(c, d) CTR_CS(a, c) CTR_CS(b, d) CTR_CS(b, c)
+#undef CTR_CS
+}
+
+// Per (view, voxel column) footprint.
+struct Footprint {
+    float sfc;            // fractional column index of the column centre's tau
+    float u0, u1, u2, u3; // sorted corner taus relative to the centre, in columns
+    float inv2r1, halfr2, inv2r2;  // trapezoid ramp constants (0 if degenerate)
+    float lxy;            // transaxial amplitude L_xy
+    float B0, H;          // axial: voxel k spans row units [B0 + k H, B0 + (k+1) H]
+};
+
+// atan2 of a small angle given (sin-like, cos-like) components.
+__device__ __forceinline__ float small_atan2(float y, float x) { return atan2f(y, x); }
+
+// view: (cos beta, sin beta, z_s)
+template <bool ARC>
+__device__ __forceinline__ void ct_footprint(const DGeom& G, float cb, float sb, float zs, int i, int j,
+                                             Footprint& f) {
+    const float cx = fmaf((float)i, G.dx, G.x0);
+    const float cy = fmaf((float)j, G.dy, G.y0);
+    const float rx = cx - G.dso * cb;
+    const float ry = cy - G.dso * sb;
+    // frame of the view: a along e_c = -(cos,sin), b along e_u = (-sin, cos)
+    const float a = -(rx * cb + ry * sb);
+    const float b = ry * cb - rx * sb;
+    const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
+    // corner offsets (+-hx, +-hy) in (a, b): da = -(ex cb + ey sb), db = ey cb - ex sb
+    const float da1 = hx * cb, da2 = hy * sb;   // da = -(+-da1 +- da2)
+    const float db1 = hx * sb, db2 = hy * cb;   // db = (+-db2) - (+-db1)
+    float t[4];
+    float tc;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const float sx = (q & 1) ? 1.f : -1.f;
+        const float sy = (q & 2) ? 1.f : -1.f;
+        const float dA = -(sx * da1 + sy * da2);
+        const float dB = sy * db2 - sx * db1;
+        if (ARC) {
+            // angle(p_k) - angle(p_c) = atan2(a db - b da, a (a + da) + b (b + db))
+            const float cr = a * dB - b * dA;
+            const float dt_ = fmaf(a, a + dA, b * (b + dB));
+            t[q] = atan2f(cr, dt_);
+        } else {
+            // Dsd (b+db)/(a+da) - Dsd b/a = Dsd (db a - b da) / (a (a + da))
+            t[q] = G.dsd * (dB * a - b * dA) / (a * (a + dA));
+        }
+    }
+    tc = ARC ? atan2f(b, a) : G.dsd * b / a;
+    sort4(t[0], t[1], t[2], t[3]);
+    f.u0 = t[0] * G.inv_delta;
+    f.u1 = t[1] * G.inv_delta;
+    f.u2 = t[2] * G.inv_delta;
+    f.u3 = t[3] * G.inv_delta;
+    f.sfc = fmaf(tc, G.inv_delta, G.s_c0);
+    const float r1 = f.u1 - f.u0, r2 = f.u3 - f.u2;
+    f.inv2r1 = r1 > kRampEps ? 0.5f / r1 : 0.f;
+    f.halfr2 = r2 > kRampEps ? 0.5f * r2 : 0.f;
+    f.inv2r2 = r2 > kRampEps ? 0.5f / r2 : 0.f;
+    // L_xy = min(dx/|d_x|, dy/|d_y|) with d = (rx, ry)/|r|
+    const float rn = sqrtf(rx * rx + ry * ry);
+    const float arx = fabsf(rx), ary = fabsf(ry);
+    const float lx = arx > 0.f ? G.dx * rn / arx : 3.0e38f;
+    const float ly = ary > 0.f ? G.dy * rn / ary : 3.0e38f;
+    f.lxy = fminf(lx, ly);
+    // axial magnification: flat Dsd/a, arc Dsd/|r|; row units u = t/dt + t_c0p
+    const float mag = ARC ? G.dsd / rn : G.dsd / a;
+    const float mdt = mag * G.inv_dt;
+    f.H = G.dz * mdt;
+    f.B0 = fmaf(G.z0 - 0.5f * G.dz - zs, mdt, G.t_c0p);
+}
+
+// Antiderivative of the unit-height trapezoid at column-relative coordinate u
+// (SURVEY.md 8c.5), in column units.
+__device__ __forceinline__ float trap_T(const Footprint& f, float u) {
+    const float p1 = fminf(fmaxf(u, f.u0), f.u1) - f.u0;
+    const float fl = fminf(fmaxf(u, f.u1), f.u2) - f.u1;
+    const float p2 = f.u3 - fminf(fmaxf(u, f.u2), f.u3);
+    return p1 * p1 * f.inv2r1 + fl + (f.halfr2 - p2 * p2 * f.inv2r2);
+}
+
+// F1 of column s: mean of the trapezoid over the column.
+__device__ __forceinline__ float sf_F1(const Footprint& f, int s) {
+    const float e0 = ((float)s - 0.5f) - f.sfc;
+    const float e1 = ((float)s + 0.5f) - f.sfc;
+    return trap_T(f, e1) - trap_T(f, e0);
+}
+
+__device__ __forceinline__ float voxel_b(const Footprint& f, int k) { return fmaf((float)k, f.H, f.B0); }
+
+// L_z(s, t): 3-D path length per unit in-plane length of ray (s, t).
+template <bool ARC>
+__device__ __forceinline__ float ray_Lz(const DGeom& G, int s, int t) {
+    const float th = ((float)t + 0.5f - G.t_c0p) * G.dt;
+    if (ARC) {
+        return sqrtf(fmaf(th, th, G.dsd * G.dsd)) / G.dsd;
+    } else {
+        const float sg = ((float)s - G.s_c0) * G.delta;
+        const float q = fmaf(sg, sg, G.dsd * G.dsd);
+        return sqrtf((q + th * th) / q);
+    }
+}
+
+}  // namespace ctr

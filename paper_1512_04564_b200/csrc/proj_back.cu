@@ -1,0 +1,174 @@
+// proj_back.cu — K3 (+K5 epilogue): voxel-driven separable-footprint
+// back-projection, a gather over the subset's views.
+//
+// Thread = one voxel column (i, j) and a z-chunk of BK_KZ voxels (register
+// accumulators); block = 32 x BK_Y columns (32 consecutive x in a warp, so a
+// warp's sinogram reads hit consecutive detector columns).  Per view the
+// thread evaluates the column's footprint once (ct_footprint, shared with the
+// forward kernel), keeps F1 of its <= kMaxCells columns in a per-thread
+// shared-memory slot, forms the row sums rs(t) = L_xy sum_s F1(s) r[t][s] of
+// the rows its chunk projects to, then distributes them to its voxels with
+// the exact overlaps F2 (same boundary arithmetic as the forward's merge).
+//
+// Epilogues (Algorithm 1; htilde form):
+//   BK_WRITE   out = scale * A'r          BK_ACCUM out += scale * A'r
+//   BK_INIT    zeta = M A'r;  g = zeta; htilde = zeta         (line 1)
+//   BK_UPDATE  zeta = M A'r;  g = rho/(rho+1)(alpha zeta + (1-alpha) g) + g/(rho+1);
+//              htilde += alpha zeta                            (lines 6-8)
+#include "kernels.cuh"
+
+namespace ctr {
+
+constexpr int BK_Y = 4;
+constexpr int BK_BS = 32 * BK_Y;
+constexpr int BK_KZ = 16;
+constexpr int BK_RMAX = 48;  // rows buffered per pass (more rows => several passes)
+
+template <bool ARC, int DIM, int EPI, bool LZ>
+__global__ void __launch_bounds__(BK_BS)
+k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+       const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
+       float* __restrict__ htbuf) {
+    __shared__ float f1s[kMaxCells][BK_BS];
+    __shared__ float rsb[(DIM == 3) ? BK_RMAX : 1][BK_BS];
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * BK_Y + threadIdx.y;
+    const int k0 = blockIdx.z * BK_KZ;
+    if (i >= G.nx || j >= G.ny) return;
+    const Views V = select_views(ctl, vsel);
+    const int nt = (DIM == 3) ? G.nt : 1;
+    const int kz = (DIM == 3) ? min(BK_KZ, G.nz - k0) : 1;
+
+    float acc[BK_KZ];
+#pragma unroll
+    for (int q = 0; q < BK_KZ; q++) acc[q] = 0.f;
+
+    for (int vi = 0; vi < V.count; vi++) {
+        const int v = V.start + vi * V.stride;
+        const float4 vw = __ldg(&vtab[v]);
+        Footprint f;
+        ct_footprint<ARC>(G, vw.x, vw.y, vw.z, i, j, f);
+        int t0 = 0, t1 = 0;
+        if (DIM == 3) {
+            const float clo = voxel_b(f, k0), chi = voxel_b(f, k0 + kz);
+            t0 = max((int)floorf(clo), 0);
+            t1 = min((int)ceilf(chi), nt) - 1;
+            if (t0 > t1) continue;
+        }
+        // detector columns under the footprint
+        int slo = (int)floorf(f.sfc + f.u0 + 0.5f);
+        int shi = (int)floorf(f.sfc + f.u3 + 0.5f);
+        slo = max(slo, 0);
+        shi = min(shi, G.ns - 1);
+        int nc = shi - slo + 1;
+        if (nc <= 0) continue;
+        if (nc > kMaxCells) nc = kMaxCells;  // excluded at ct_geom_create (footprint bound)
+        {
+            float Tprev = trap_T(f, ((float)slo - 0.5f) - f.sfc);
+            for (int q = 0; q < nc; q++) {
+                const float Tn = trap_T(f, ((float)(slo + q) + 0.5f) - f.sfc);
+                f1s[q][tid] = (Tn - Tprev) * f.lxy;
+                Tprev = Tn;
+            }
+        }
+        const float* __restrict__ pv = proj + (size_t)vi * nt * G.ns + slo;
+        if (DIM != 3) {
+            float rs = 0.f;
+            for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pv[q]), rs);
+            acc[0] += rs;
+            continue;
+        }
+        for (int tw = t0; tw <= t1; tw += BK_RMAX) {
+            const int twe = min(t1, tw + BK_RMAX - 1);
+            for (int t = tw; t <= twe; t++) {
+                const float* __restrict__ pr = pv + (size_t)t * G.ns;
+                float rs = 0.f;
+                if (LZ) {
+                    for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid] * ray_Lz<ARC>(G, slo + q, t), __ldg(&pr[q]), rs);
+                } else {
+                    for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pr[q]), rs);
+                }
+                rsb[t - tw][tid] = rs;
+            }
+#pragma unroll
+            for (int q = 0; q < BK_KZ; q++) {
+                if (q < kz) {
+                    const float lo = voxel_b(f, k0 + q), hi = voxel_b(f, k0 + q + 1);
+                    const int ta = max((int)floorf(lo), tw);
+                    const int tb = min((int)ceilf(hi) - 1, twe);
+                    float a = acc[q];
+                    for (int t = ta; t <= tb; t++) {
+                        const float ov = fminf(hi, (float)(t + 1)) - fmaxf(lo, (float)t);
+                        a = fmaf(ov, rsb[t - tw][tid], a);
+                    }
+                    acc[q] = a;
+                }
+            }
+        }
+    }
+
+    // epilogue
+    float rho = 0.f, alpha = 0.f;
+    if (EPI == BK_UPDATE) {
+        rho = rho_of_k(ctl);
+        alpha = ctl->alpha;
+    }
+#pragma unroll
+    for (int q = 0; q < BK_KZ; q++) {
+        if (q < kz) {
+            const size_t idx = (size_t)(k0 + q) * G.nxy + (size_t)j * G.nx + i;
+            const float z = scale * acc[q];
+            if (EPI == BK_WRITE) {
+                out[idx] = z;
+            } else if (EPI == BK_ACCUM) {
+                out[idx] += z;
+            } else if (EPI == BK_INIT) {
+                gbuf[idx] = z;
+                htbuf[idx] = z;
+            } else {
+                const float gv = gbuf[idx];
+                const float inv = 1.f / (rho + 1.f);
+                gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
+                htbuf[idx] = fmaf(alpha, z, htbuf[idx]);
+            }
+        }
+    }
+}
+
+template <bool ARC, int DIM>
+static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
+                          float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
+    dim3 block(32, BK_Y);
+    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, DIM == 3 ? (G.nz + BK_KZ - 1) / BK_KZ : 1);
+    switch (epi) {
+        case BK_WRITE:
+            if (lz) k_back<ARC, DIM, BK_WRITE, true><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back<ARC, DIM, BK_WRITE, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_ACCUM:
+            if (lz) k_back<ARC, DIM, BK_ACCUM, true><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back<ARC, DIM, BK_ACCUM, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_INIT:
+            k_back<ARC, DIM, BK_INIT, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        default:
+            k_back<ARC, DIM, BK_UPDATE, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+    }
+}
+
+void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
+                 int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s) {
+    if (G.arc) {
+        if (G.dim == 3) back_dispatch<true, 3>(G, vtab, ctl, v, proj, scale, epi, apply_lz, out, g, ht, s);
+        else back_dispatch<true, 2>(G, vtab, ctl, v, proj, scale, epi, false, out, g, ht, s);
+    } else {
+        if (G.dim == 3) back_dispatch<false, 3>(G, vtab, ctl, v, proj, scale, epi, apply_lz, out, g, ht, s);
+        else back_dispatch<false, 2>(G, vtab, ctl, v, proj, scale, epi, false, out, g, ht, s);
+    }
+    launches_add(1);
+}
+
+}  // namespace ctr

@@ -1,0 +1,212 @@
+// proj_fwd.cu — K1+K2: ray-driven separable-footprint forward projection with
+// the statistically weighted residual fused in the epilogue.
+//
+// One thread owns one detector column s of one view (a "cell" in 2-D, a
+// column of nt rows in 3-D); a block owns FWD_BS consecutive columns of one
+// view.  The thread walks the fan wedge of its column along the dominant
+// axis of its central ray, tests each candidate voxel column against the two
+// edge rays (support-function test of the square against the two
+// half-planes), evaluates the SF footprint of the surviving columns
+// (ct_footprint, the same function the back-projector uses) and, in 3-D,
+// resamples the voxel column onto the detector rows by a merge of the voxel
+// and row boundaries (exact overlaps, F2).  Row sums accumulate in a
+// per-thread shared-memory column acc[t][tid]: a gather — no atomics, no
+// cross-thread writes, no __syncthreads.
+//
+// Epilogue (Eq. 36 applied implicitly):
+//   FWD_PLAIN  p = L_z q
+//   FWD_RESID  r = L_z w (L_z q - y)     -> back-projector needs no L_z
+//   FWD_ONES_W r = L_z w (L_z A0 1)      (D_L = A'WA1)
+#include "kernels.cuh"
+
+namespace ctr {
+
+constexpr int FWD_BS = 128;
+
+template <bool ARC, int DIM, int MODE>
+__global__ void __launch_bounds__(FWD_BS)
+k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+      const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
+      const float* __restrict__ w, float* __restrict__ out) {
+    extern __shared__ float acc[];  // [nt][FWD_BS] in 3-D
+    const Views V = select_views(ctl, vsel);
+    const int vi = blockIdx.y;
+    if (vi >= V.count) return;
+    const int v = V.start + vi * V.stride;
+    const int tid = threadIdx.x;
+    const int s = blockIdx.x * FWD_BS + tid;
+    if (s >= G.ns) return;
+    constexpr bool ONES = (MODE == FWD_ONES_W);
+    const float* __restrict__ x = xa;
+    if (ctl) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
+
+    const float4 vw = __ldg(&vtab[v]);
+    const float cb = vw.x, sb = vw.y, zs = vw.z;
+    const float Sx = G.dso * cb, Sy = G.dso * sb;
+    const int nt = (DIM == 3) ? G.nt : 1;
+    if (DIM == 3) {
+        for (int t = 0; t < nt; t++) acc[t * FWD_BS + tid] = 0.f;
+    }
+    float q2d = 0.f;
+
+    // edge rays of column s: tau_l, tau_r; central ray tau_m
+    const float tl = ((float)s - 0.5f - G.s_c0) * G.delta;
+    const float tr = ((float)s + 0.5f - G.s_c0) * G.delta;
+    const float tm = ((float)s - G.s_c0) * G.delta;
+    float cal, cul, car, cur_, cam, cum;
+    if (ARC) {
+        sincosf(tl, &cul, &cal);
+        sincosf(tr, &cur_, &car);
+        sincosf(tm, &cum, &cam);
+    } else {
+        cal = car = cam = G.dsd;
+        cul = tl; cur_ = tr; cum = tm;
+    }
+    // world directions d = ca e_c + cu e_u, e_c = (-cb, -sb), e_u = (-sb, cb)
+    const float dlx = -cal * cb - cul * sb, dly = -cal * sb + cul * cb;
+    const float drx = -car * cb - cur_ * sb, dry = -car * sb + cur_ * cb;
+    const float dmx = -cam * cb - cum * sb, dmy = -cam * sb + cum * cb;
+    // inward normals: tau > tau_l <=> nl.(P-S) > 0 ; tau < tau_r <=> nr.(P-S) > 0
+    const float nlx = -cal * sb + cul * cb, nly = cal * cb + cul * sb;
+    const float nrx = car * sb - cur_ * cb, nry = -car * cb - cur_ * sb;
+    const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
+    const float suppl = fabsf(nlx) * hx + fabsf(nly) * hy;
+    const float suppr = fabsf(nrx) * hx + fabsf(nry) * hy;
+    const float tol_l = 1e-4f * suppl, tol_r = 1e-4f * suppr;
+    const bool xstep = fabsf(dmx) >= fabsf(dmy);
+
+    auto visit = [&](int i, int j) {
+        const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
+        const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
+        if (fmaf(nlx, cx, nly * cy) + suppl < -tol_l) return;
+        if (fmaf(nrx, cx, nry * cy) + suppr < -tol_r) return;
+        Footprint f;
+        ct_footprint<ARC>(G, cb, sb, zs, i, j, f);
+        const float F1 = sf_F1(f, s);
+        if (!(F1 > 0.f)) return;
+        const float L = f.lxy * F1;
+        if (DIM != 3) {
+            q2d = fmaf(L, ONES ? 1.f : __ldg(&x[(size_t)j * G.nx + i]), q2d);
+            return;
+        }
+        // merge voxel boundaries b_k = B0 + k H with row boundaries t (row units)
+        const float ulo = fmaxf(f.B0, 0.f);
+        const float uhi = fminf(voxel_b(f, G.nz), (float)nt);
+        if (!(ulo < uhi)) return;
+        int k = (int)floorf((ulo - f.B0) / f.H);
+        k = min(max(k, 0), G.nz - 1);
+        while (k + 1 < G.nz && voxel_b(f, k + 1) <= ulo) k++;
+        while (k > 0 && voxel_b(f, k) > ulo) k--;
+        int t = min((int)floorf(ulo), nt - 1);
+        const float* __restrict__ xc = x + (size_t)j * G.nx + i;
+        float xv = ONES ? 1.f : __ldg(&xc[(size_t)k * G.nxy]);
+        float pos = ulo, cur = 0.f;
+        while (true) {
+            const float bk1 = voxel_b(f, k + 1);
+            const float tn = (float)(t + 1);
+            const float nxt = fminf(fminf(bk1, tn), uhi);
+            cur = fmaf(nxt - pos, xv, cur);
+            pos = nxt;
+            if (nxt >= uhi) break;
+            if (tn <= bk1) {
+                acc[t * FWD_BS + tid] = fmaf(L, cur, acc[t * FWD_BS + tid]);
+                cur = 0.f;
+                t++;
+            }
+            if (bk1 <= tn) {
+                k++;
+                if (!ONES) xv = __ldg(&xc[(size_t)k * G.nxy]);
+            }
+        }
+        acc[t * FWD_BS + tid] = fmaf(L, cur, acc[t * FWD_BS + tid]);
+    };
+
+    if (xstep) {
+        const float kl = dly / dlx, kr = dry / drx;
+        const float sgn = dlx > 0.f ? 1.f : -1.f;
+        for (int i = 0; i < G.nx; i++) {
+            const float xc = fmaf((float)i, G.dx, G.x0);
+            const float xa_ = xc - hx - Sx, xb_ = xc + hx - Sx;
+            if (xa_ * sgn <= 0.f || xb_ * sgn <= 0.f) continue;  // behind the source
+            const float y1 = fmaf(xa_, kl, Sy), y2 = fmaf(xb_, kl, Sy);
+            const float y3 = fmaf(xa_, kr, Sy), y4 = fmaf(xb_, kr, Sy);
+            const float ymin = fminf(fminf(y1, y2), fminf(y3, y4));
+            const float ymax = fmaxf(fmaxf(y1, y2), fmaxf(y3, y4));
+            const float fy0 = (ymin - G.y0) / G.dy + 0.5f, fy1 = (ymax - G.y0) / G.dy + 0.5f;
+            if (fy1 < -1.f || fy0 > (float)G.ny + 1.f) continue;
+            const int jlo = max((int)floorf(fy0) - 1, 0);
+            const int jhi = min((int)floorf(fy1) + 1, G.ny - 1);
+            for (int j = jlo; j <= jhi; j++) visit(i, j);
+        }
+    } else {
+        const float kl = dlx / dly, kr = drx / dry;
+        const float sgn = dly > 0.f ? 1.f : -1.f;
+        for (int j = 0; j < G.ny; j++) {
+            const float yc = fmaf((float)j, G.dy, G.y0);
+            const float ya_ = yc - hy - Sy, yb_ = yc + hy - Sy;
+            if (ya_ * sgn <= 0.f || yb_ * sgn <= 0.f) continue;
+            const float x1 = fmaf(ya_, kl, Sx), x2 = fmaf(yb_, kl, Sx);
+            const float x3 = fmaf(ya_, kr, Sx), x4 = fmaf(yb_, kr, Sx);
+            const float xmin = fminf(fminf(x1, x2), fminf(x3, x4));
+            const float xmax = fmaxf(fmaxf(x1, x2), fmaxf(x3, x4));
+            const float fx0 = (xmin - G.x0) / G.dx + 0.5f, fx1 = (xmax - G.x0) / G.dx + 0.5f;
+            if (fx1 < -1.f || fx0 > (float)G.nx + 1.f) continue;
+            const int ilo = max((int)floorf(fx0) - 1, 0);
+            const int ihi = min((int)floorf(fx1) + 1, G.nx - 1);
+            for (int i = ilo; i <= ihi; i++) visit(i, j);
+        }
+    }
+
+    // epilogue: amplitude L_z, residual weighting (Eq. 36), write (coalesced over s)
+    for (int t = 0; t < nt; t++) {
+        const float q = (DIM == 3) ? acc[t * FWD_BS + tid] : q2d;
+        const float lz = (DIM == 3) ? ray_Lz<ARC>(G, s, t) : 1.f;
+        const size_t o = ((size_t)vi * nt + t) * G.ns + s;
+        const float p = lz * q;
+        if (MODE == FWD_PLAIN) {
+            out[o] = p;
+        } else {
+            const size_t a = ((size_t)v * nt + t) * G.ns + s;
+            const float wv = w ? __ldg(&w[a]) : 1.f;
+            if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldg(&y[a]));
+            else out[o] = lz * wv * p;
+        }
+    }
+}
+
+template <bool ARC, int DIM>
+static void fwd_dispatch_mode(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
+                              const float* xa, const float* xb, const float* y, const float* w, float* out,
+                              int mode, cudaStream_t s) {
+    dim3 grid((G.ns + FWD_BS - 1) / FWD_BS, max_count);
+    size_t smem = (DIM == 3) ? (size_t)G.nt * FWD_BS * sizeof(float) : 0;
+    switch (mode) {
+        case FWD_PLAIN:
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_fwd<ARC, DIM, FWD_PLAIN><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+            break;
+        case FWD_RESID:
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_fwd<ARC, DIM, FWD_RESID><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+            break;
+        default:
+            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_ONES_W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_fwd<ARC, DIM, FWD_ONES_W><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+            break;
+    }
+}
+
+void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
+                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s) {
+    if (max_count <= 0) return;
+    if (G.arc) {
+        if (G.dim == 3) fwd_dispatch_mode<true, 3>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        else fwd_dispatch_mode<true, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+    } else {
+        if (G.dim == 3) fwd_dispatch_mode<false, 3>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        else fwd_dispatch_mode<false, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+    }
+    launches_add(1);
+}
+
+}  // namespace ctr

@@ -1,0 +1,228 @@
+// reg_update.cu — K4 regulariser stencil (Eq. 35) and the
+// fused Algorithm 1 x-update (lines 4-5), plus the small
+// elementwise kernels of the solver (dist-path g/htilde update, advance of
+// the Eq. 37 counter, htilde -> h, finiteness / RMS check).
+//
+// grad_j = sum_n beta_{d(j,n)} kappa_j kappa_n phi'(x_j - x_n)
+// D_R,j  = 2 sum_n beta_{d(j,n)} kappa_j kappa_n omega(x_j - x_n),  omega = phi'(t)/t
+// over the in-volume neighbours n (26 in 3-D, 8 in 2-D).
+//
+// Update (htilde = D_L x - h):
+//   s   = rho htilde + (1 - rho) g
+//   x+  = clamp(x - (s + grad)/(rho D_L + D_R), box)   (denominator 0 keeps x)
+//   htilde_partial = (1 - alpha) (D_L (x+ - x) + htilde)   (completed by the
+//                     back-projection epilogue: htilde+ = htilde_partial + alpha zeta)
+#include "kernels.cuh"
+
+namespace ctr {
+
+__constant__ int c_dirs[13][3] = {
+    {1, 0, 0}, {0, 1, 0}, {1, 1, 0}, {1, -1, 0},
+    {0, 0, 1}, {1, 0, 1}, {-1, 0, 1}, {0, 1, 1}, {0, -1, 1},
+    {1, 1, 1}, {-1, 1, 1}, {1, -1, 1}, {-1, -1, 1},
+};
+
+template <int POT>
+__device__ __forceinline__ void potential(float t, float inv_delta, float& dphi, float& om) {
+    if (POT == 0) {          // quadratic
+        dphi = t;
+        om = 1.f;
+    } else if (POT == 1) {   // hyperbola
+        const float u = t * inv_delta;
+        om = rsqrtf(fmaf(u, u, 1.f));
+        dphi = t * om;
+    } else {                 // Fair
+        om = 1.f / fmaf(fabsf(t), inv_delta, 1.f);
+        dphi = t * om;
+    }
+}
+
+template <int POT, int NDIRS, bool KAPPA>
+__device__ __forceinline__ void stencil(const DGeom& G, const RegParams& rp, const float* __restrict__ x,
+                                        const float* __restrict__ kappa, int i, int j, int k, size_t idx,
+                                        float xv, float& grad, float& curv) {
+    const float kj = KAPPA ? __ldg(&kappa[idx]) : 1.f;
+    float gs = 0.f, cs = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIRS; d++) {
+        const int ox = c_dirs[d][0], oy = c_dirs[d][1], oz = c_dirs[d][2];
+        const long long off = (long long)oz * G.nxy + (long long)oy * G.nx + ox;
+        const float b = rp.beta[d];
+#pragma unroll
+        for (int sgn = 0; sgn < 2; sgn++) {
+            const int si = sgn ? -1 : 1;
+            const int ni = i + si * ox, nj = j + si * oy, nk = k + si * oz;
+            if (ni < 0 || nj < 0 || nk < 0 || ni >= G.nx || nj >= G.ny || nk >= G.nz) continue;
+            const size_t nb = (size_t)((long long)idx + si * off);
+            const float wgt = KAPPA ? b * kj * __ldg(&kappa[nb]) : b;
+            float dphi, om;
+            potential<POT>(xv - __ldg(&x[nb]), rp.inv_delta, dphi, om);
+            gs = fmaf(wgt, dphi, gs);
+            cs = fmaf(wgt, om, cs);
+        }
+    }
+    grad = gs;
+    curv = 2.f * cs;
+}
+
+template <int POT, int NDIRS, bool KAPPA>
+__global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float* __restrict__ x,
+                                             const float* __restrict__ kappa, float* __restrict__ grad,
+                                             float* __restrict__ curv) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= G.nx || j >= G.ny) return;
+    const size_t idx = (size_t)k * G.nxy + (size_t)j * G.nx + i;
+    float gr, cv;
+    stencil<POT, NDIRS, KAPPA>(G, rp, x, kappa, i, j, k, idx, __ldg(&x[idx]), gr, cv);
+    grad[idx] = gr;
+    if (curv) curv[idx] = cv;
+}
+
+template <int POT, int NDIRS, bool KAPPA>
+__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
+                                                float* xb, const float* __restrict__ dl,
+                                                const float* __restrict__ g, float* __restrict__ ht,
+                                                const float* __restrict__ kappa, float box_lo, float box_hi) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int k = blockIdx.z;
+    if (i >= G.nx || j >= G.ny) return;
+    const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
+    const float* __restrict__ x = odd ? xb : xa;
+    float* __restrict__ xn = odd ? xa : xb;
+    const size_t idx = (size_t)k * G.nxy + (size_t)j * G.nx + i;
+    const float xv = x[idx];
+    float gr, cv;
+    stencil<POT, NDIRS, KAPPA>(G, rp, x, kappa, i, j, k, idx, xv, gr, cv);
+    const float rho = rho_of_k(ctl);
+    const float alpha = ctl->alpha;
+    const float d = __ldg(&dl[idx]);
+    const float htv = ht[idx];
+    const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
+    const float den = fmaf(rho, d, cv);
+    float xnew = xv;
+    if (den > 0.f) xnew = fminf(fmaxf(xv - (s + gr) / den, box_lo), box_hi);
+    xn[idx] = xnew;
+    ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+}
+
+template <int POT, int NDIRS>
+static void reg_dispatch(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad,
+                         float* curv, cudaStream_t s) {
+    dim3 block(32, 8), grid((G.nx + 31) / 32, (G.ny + 7) / 8, G.nz);
+    if (kappa) k_reg<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, x, kappa, grad, curv);
+    else k_reg<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, x, kappa, grad, curv);
+}
+
+void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad, float* curv,
+                cudaStream_t s) {
+    const bool d4 = rp.n_dirs == 4;
+    switch (rp.potential) {
+        case 0: d4 ? reg_dispatch<0, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<0, 13>(G, rp, x, kappa, grad, curv, s); break;
+        case 1: d4 ? reg_dispatch<1, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<1, 13>(G, rp, x, kappa, grad, curv, s); break;
+        default: d4 ? reg_dispatch<2, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<2, 13>(G, rp, x, kappa, grad, curv, s); break;
+    }
+    launches_add(1);
+}
+
+template <int POT, int NDIRS>
+static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
+                         const float* g, float* ht, const float* kappa, float lo, float hi, cudaStream_t s) {
+    dim3 block(32, 8), grid((G.nx + 31) / 32, (G.ny + 7) / 8, G.nz);
+    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi);
+    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi);
+}
+
+void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
+                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, cudaStream_t s) {
+    const bool d4 = rp.n_dirs == 4;
+    switch (rp.potential) {
+        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
+        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
+        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
+    }
+    launches_add(1);
+}
+
+// ---- small elementwise kernels ----
+__global__ void k_gh_update(long long n, const Ctl* __restrict__ ctl, const float* __restrict__ zeta, float* g,
+                            float* ht) {
+    const float rho = rho_of_k(ctl), alpha = ctl->alpha, inv = 1.f / (rho + 1.f);
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const float z = zeta[idx], gv = g[idx];
+        g[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
+        ht[idx] = fmaf(alpha, z, ht[idx]);
+    }
+}
+
+__global__ void k_init_from_zeta(long long n, const float* __restrict__ zeta, float* g, float* ht) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        g[idx] = zeta[idx];
+        ht[idx] = zeta[idx];
+    }
+}
+
+__global__ void k_advance(Ctl* ctl) { ctl->k += 1; }
+
+__global__ void k_state_h(long long n, const float* __restrict__ dl, const float* __restrict__ x,
+                          const float* __restrict__ ht, float* h) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x)
+        h[idx] = fmaf(dl[idx], x[idx], -ht[idx]);
+}
+
+__global__ void k_check(long long n, const float* __restrict__ x, const float* __restrict__ xref, int* flag,
+                        double* dsum) {
+    double acc = 0.0;
+    int bad = 0;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const float v = x[idx];
+        if (!isfinite(v)) bad = 1;
+        if (xref) {
+            const double d = (double)v - (double)xref[idx];
+            acc += d * d;
+        }
+    }
+    // warp reduce then one atomic per warp (a scalar diagnostic, not the data path)
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_down_sync(0xffffffffu, acc, o);
+        bad |= __shfl_down_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (bad) atomicOr(flag, 1);
+        if (xref) atomicAdd(dsum, acc);
+    }
+}
+
+static int grid_for(long long n) {
+    long long b = (n + 255) / 256;
+    return (int)(b < 148LL * 16 ? b : 148LL * 16);
+}
+
+void launch_gh_update(const DGeom& G, const Ctl* ctl, const float* zeta, float* g, float* ht, cudaStream_t s) {
+    k_gh_update<<<grid_for(G.nvox), 256, 0, s>>>(G.nvox, ctl, zeta, g, ht);
+    launches_add(1);
+}
+void launch_init_from_zeta(const DGeom& G, const float* zeta, float* g, float* ht, cudaStream_t s) {
+    k_init_from_zeta<<<grid_for(G.nvox), 256, 0, s>>>(G.nvox, zeta, g, ht);
+    launches_add(1);
+}
+void launch_advance(Ctl* ctl, cudaStream_t s) {
+    k_advance<<<1, 1, 0, s>>>(ctl);
+    launches_add(1);
+}
+void launch_state_h(const DGeom& G, const float* dl, const float* x, const float* ht, float* h, cudaStream_t s) {
+    k_state_h<<<grid_for(G.nvox), 256, 0, s>>>(G.nvox, dl, x, ht, h);
+    launches_add(1);
+}
+void launch_check(const DGeom& G, const float* x, const float* xref, int* flag, double* dsum, cudaStream_t s) {
+    k_check<<<grid_for(G.nvox), 256, 0, s>>>(G.nvox, x, xref, flag, dsum);
+    launches_add(1);
+}
+
+}  // namespace ctr

@@ -1,0 +1,80 @@
+"""Device-side setup for one reconstruction: allocation + C-ABI calls only.
+
+`Recon` owns the torch CUDA tensors (sinogram y, weights w, D_L, state x, g,
+htilde, workspace) and the ct_geom handle, and calls the C-ABI in the order of
+Algorithm 1: D_L once, then
+oslalm_relaxed_solve for as many sub-iterations as asked (line 1 runs inside
+the first call, k == 0).  No arithmetic of the method runs in Python.
+"""
+import math
+
+import torch
+
+from . import ctrecon as C
+
+
+class Recon:
+    def __init__(self, geom, reg, solver, y, w, x0, kappa=None, device=0, dist=None, stream=None):
+        """geom/reg/solver: dicts as in synth/configs.py; y, w: (na, nt, ns);
+        x0: (nz, ny, nx).  Arrays may be numpy/torch of any float dtype; they
+        are copied to float32 device tensors."""
+        self.dev = torch.device("cuda", device)
+        self.geom = geom
+        self.desc = C.geom_desc(geom)
+        self.h = C.ct_geom_create(self.desc, device)
+        self.dist = dist
+        self.stream = stream
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.y = torch.as_tensor(y).to(**f32).contiguous()
+        self.w = torch.as_tensor(w).to(**f32).contiguous() if w is not None else None
+        self.kappa = torch.as_tensor(kappa).to(**f32).contiguous() if kappa is not None else None
+        self.x = torch.as_tensor(x0).to(**f32).contiguous().clone()
+        self.g = torch.zeros_like(self.x)
+        self.htilde = torch.zeros_like(self.x)
+        self.reg = C.reg_desc(reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"])
+        self.params = C.params(solver["M"], solver["alpha"],
+                               C.RHO_FIXED if solver.get("rho_mode") == "fixed" else C.RHO_CONTINUATION,
+                               solver.get("rho_fixed", 0.0),
+                               C.INIT_FULL if solver.get("init_grad") == "full" else C.INIT_LAST_SUBSET,
+                               solver.get("box_lo", 0.0), solver.get("box_hi", math.inf))
+        nbytes = C.oslalm_workspace_size(self.h, self.params, dist)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+        self.state = C.make_state(self.x, self.g, self.htilde, 0)
+        self.dl = None
+
+    def compute_DL(self):
+        """D_L = diag(A'WA1) over all views (ct_sqs_diag), once per reconstruction."""
+        self.dl = torch.empty_like(self.x)
+        C.ct_sqs_diag(self.h, self.w, self.dl, self.ws, dist=self.dist, stream=self.stream)
+        return self.dl
+
+    def set_DL(self, dl):
+        self.dl = torch.as_tensor(dl).to(dtype=torch.float32, device=self.dev).contiguous()
+
+    def run(self, n_subiters, x_ref=None, rms=None):
+        if self.dl is None:
+            self.compute_DL()
+        C.oslalm_relaxed_solve(self.h, self.y, self.w, self.reg, self.kappa, self.dl, self.params, self.state,
+                               n_subiters, self.ws, x_ref=x_ref, rms_per_iter=rms, dist=self.dist,
+                               stream=self.stream)
+        return self.x
+
+    @property
+    def k(self):
+        return self.state.k
+
+    def paper_h(self):
+        h = torch.empty_like(self.x)
+        C.oslalm_state_h(self.h, self.dl, self.state, h, stream=self.stream)
+        return h
+
+    def close(self):
+        if self.h is not None:
+            C.ct_geom_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

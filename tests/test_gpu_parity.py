@@ -1,0 +1,256 @@
+"""GPU (CUDA path, through the C-ABI) vs oracle parity — needs a B200.
+
+Tolerances (BASELINE.json north_star): projections 1e-4
+relative L2, reconstructed images 1e-3 relative RMS after a fixed number of
+iterations; per-step traces 1e-4; GPU adjoint identity 1e-5.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import alg  # noqa: E402
+from oracle import projector as P  # noqa: E402
+from tests.geoms import KINDS, tiny  # noqa: E402
+from tests.problems import config_problem, oracle_problem, rel, synthetic_problem  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def C():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1512_04564_b200 import ctrecon
+    ctrecon.load()
+    return ctrecon
+
+
+def dev(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.float32, device="cuda")
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.double().cpu().numpy()
+
+
+GEOMS = {k: tiny(k) for k in KINDS}
+GEOMS["c1"] = None  # filled lazily from synth
+
+
+def geom_of(name):
+    if name == "c1":
+        from synth.configs import get_config
+        return get_config("c1")["geom"]
+    return GEOMS[name]
+
+
+@pytest.mark.parametrize("name", KINDS + ["c1"])
+def test_forward_back_parity(C, name):
+    g = geom_of(name)
+    rng = np.random.default_rng(7)
+    x = rng.random(P.vol_shape(g))
+    cnt = g["na"]
+    yv = rng.standard_normal(P.proj_shape(g, cnt))
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        xd = dev(x)
+        pd = torch.empty(P.proj_shape(g, cnt), dtype=torch.float32, device="cuda")
+        C.ct_forward(h, xd, C.views(0, 1, cnt), pd)
+        pf = host(pd)
+        ref = P.forward(g, x)
+        assert rel(pf, ref) <= 1e-4, rel(pf, ref)
+        bd = torch.empty_like(xd)
+        C.ct_back(h, dev(yv), C.views(0, 1, cnt), bd)
+        bk = host(bd)
+        refb = P.back(g, yv)
+        assert rel(bk, refb) <= 1e-4, rel(bk, refb)
+        # GPU adjoint identity <Ax, y> = <x, A'y>
+        lhs = float(np.sum(pf * yv))
+        rhs = float(np.sum(x * bk))
+        assert abs(lhs - rhs) <= 1e-5 * (abs(lhs) + abs(rhs)), (lhs, rhs)
+        # a strided subset, scale and accumulate
+        vv = (1, 3, (cnt - 1 + 2) // 3)
+        ps = torch.empty(P.proj_shape(g, vv[2]), dtype=torch.float32, device="cuda")
+        C.ct_forward(h, xd, C.views(*vv), ps)
+        assert rel(host(ps), P.forward(g, x, vv)) <= 1e-4
+        acc = dev(x)
+        C.ct_back(h, ps, C.views(*vv), acc, scale=2.0, accumulate=True)
+        assert rel(host(acc), x + 2.0 * P.back(g, host(ps), vv)) <= 1e-5
+    finally:
+        C.ct_geom_destroy(h)
+
+
+@pytest.mark.parametrize("name", KINDS)
+def test_sqs_diag_parity(C, name):
+    g = geom_of(name)
+    rng = np.random.default_rng(8)
+    w = rng.uniform(0.5, 2.0, P.proj_shape(g, g["na"]))
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        d = torch.empty(P.vol_shape(g), dtype=torch.float32, device="cuda")
+        ws = torch.empty(3 * g["ns"] * (g["nt"] if g["dim"] == 3 else 1) * 4 + 7, dtype=torch.uint8,
+                         device="cuda")   # 3 views per chunk: exercises chunking and a ragged tail
+        C.ct_sqs_diag(h, dev(w), d, ws)
+        ref = P.back(g, w * P.forward(g, np.ones(P.vol_shape(g))))
+        assert rel(host(d), ref) <= 1e-4
+    finally:
+        C.ct_geom_destroy(h)
+
+
+@pytest.mark.parametrize("pot", ["hyperbola", "fair", "quadratic"])
+@pytest.mark.parametrize("kind", ["fan2d_arc", "helical_arc"])
+@pytest.mark.parametrize("use_kappa", [False, True])
+def test_reg_grad_parity(C, pot, kind, use_kappa):
+    g = tiny(kind, nx=37, ny=21, nz=9) if kind == "helical_arc" else tiny(kind, nx=37, ny=21)
+    rng = np.random.default_rng(9)
+    x = 0.02 * rng.random(P.vol_shape(g))
+    kap = rng.uniform(0.5, 1.5, x.shape) if use_kappa else None
+    nd = 13 if g["dim"] == 3 else 4
+    betas = list(rng.uniform(0.5, 2.0, nd))
+    _, gr, cv = P.reg(g, pot, 0.01, betas, nd, x, kap)
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        gd = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        cd = torch.empty_like(gd)
+        C.ct_reg_grad(h, C.reg_desc(pot, 0.01, betas, nd), dev(x), gd, cd, kappa=dev(kap) if use_kappa else None)
+        assert rel(host(gd), gr) <= 1e-5
+        assert rel(host(cd), cv) <= 1e-5
+    finally:
+        C.ct_geom_destroy(h)
+
+
+def _gpu_recon(pb, dl=None):
+    from paper_1512_04564_b200.recon import Recon
+    r = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
+    if dl is None:
+        r.compute_DL()
+    else:
+        r.set_DL(dl)
+    return r
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_solve_trace_matches_oracle(C, kind):
+    """Per-step trace: x, g and htilde after sub-iterations 1, 2, 3, M, 2M."""
+    pb = synthetic_problem(tiny(kind), M=3)
+    prob = oracle_problem(pb)
+    DL = pb["DL"]
+    trace = {}
+    alg.alg1(prob, pb["x0"], 3, 1.999, 2, DL=DL, trace=trace)
+    rec = _gpu_recon(pb)
+    assert rel(host(rec.dl), DL) <= 1e-4
+    done = 0
+    for k in (1, 2, 3, 6):
+        rec.run(k - done)
+        done = k
+        xo, go, ho = trace[k]
+        assert rec.k == k
+        assert rel(host(rec.x), xo) <= 1e-4, (k, rel(host(rec.x), xo))
+        assert rel(host(rec.g), go) <= 1e-3, (k, rel(host(rec.g), go))
+        assert rel(host(rec.htilde), DL * xo - ho) <= 1e-3, k
+    rec.close()
+
+
+def test_c1_full_solve_matches_oracle(C):
+    """BASELINE configs[0]: 128^2 fan, 180 views, M = 4, 20 iterations, alpha = 1.999."""
+    pb = config_problem("c1")
+    prob = oracle_problem(pb)
+    M, iters, a = pb["solver"]["M"], pb["solver"]["iters"], pb["solver"]["alpha"]
+    xo = alg.alg1(prob, pb["x0"], M, a, iters, DL=pb["DL"])[0]
+    rec = _gpu_recon(pb)
+    rec.run(M * iters)
+    xg = host(rec.x)
+    rms = math.sqrt(np.mean((xg - xo) ** 2)) / math.sqrt(np.mean(xo ** 2))
+    assert rms <= 1e-3, rms
+    assert xg.min() >= 0.0
+    rec.close()
+
+
+def test_alpha1_and_fixed_rho_and_full_init(C):
+    pb = synthetic_problem(tiny("axial_flat"), M=4, alpha=1.0)
+    pb["solver"].update(rho_mode="fixed", rho_fixed=0.3, init_grad="full")
+    prob = oracle_problem(pb)
+    x = pb["x0"].copy()
+    g, h = alg.alg1_init(prob, x, 4, pb["DL"], init_grad="full")
+    xo, go, ho, k = alg.alg1_run(prob, x, g, h, 0, 10, 4, 1.0, pb["DL"], rho_mode="fixed", rho_fixed=0.3)
+    rec = _gpu_recon(pb)
+    rec.run(10)
+    assert rel(host(rec.x), xo) <= 1e-4
+    rec.close()
+
+
+def test_ragged_subsets_and_resume(C):
+    """M does not divide na (ragged last subsets); state resumes across calls."""
+    g = tiny("helical_arc", na=41)
+    pb = synthetic_problem(g, M=4)
+    prob = oracle_problem(pb)
+    trace = {}
+    alg.alg1(prob, pb["x0"], 4, 1.999, 3, DL=pb["DL"], trace=trace)
+    rec = _gpu_recon(pb)
+    for n in (1, 4, 2, 5):
+        rec.run(n)
+    assert rec.k == 12
+    assert rel(host(rec.x), trace[12][0]) <= 1e-4
+    rec.close()
+
+
+def test_zero_data_zero_init_stays_zero(C):
+    pb = synthetic_problem(tiny("fan2d_arc"))
+    pb["y"] = np.zeros_like(pb["y"])
+    pb["x0"] = np.zeros_like(pb["x0"])
+    rec = _gpu_recon(pb)
+    rec.run(7)
+    assert float(rec.x.abs().max()) == 0.0
+    rec.close()
+
+
+def test_errors_have_no_side_effects(C):
+    g = tiny("fan2d_arc")
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        x = torch.zeros(P.vol_shape(g), dtype=torch.float32, device="cuda")
+        p = torch.full(P.proj_shape(g, 2), 7.0, dtype=torch.float32, device="cuda")
+        with pytest.raises(C.CtError) as e:
+            C.ct_forward(h, x, C.views(g["na"] - 1, 1, 2), p)   # runs past the last view
+        assert e.value.status == C.CT_E_SHAPE
+        assert float(p.min()) == 7.0
+        pb = synthetic_problem(g)
+        from paper_1512_04564_b200.recon import Recon
+        for bad in (dict(alpha=2.0), dict(alpha=0.5), dict(M=0), dict(M=g["na"] + 1)):
+            s = dict(pb["solver"], **bad)
+            with pytest.raises(C.CtError) as e:
+                Recon(g, pb["reg"], s, pb["y"], pb["w"], pb["x0"])
+            assert e.value.status == C.CT_E_CONFIG
+        bad_reg = dict(pb["reg"], delta=0.0)
+        r = Recon(g, pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
+        r.compute_DL()
+        r.reg = C.reg_desc("hyperbola", 0.0, bad_reg["betas"], 4)
+        x_before = r.x.clone()
+        with pytest.raises(C.CtError) as e:
+            r.run(3)
+        assert e.value.status == C.CT_E_CONFIG and r.k == 0 and torch.equal(r.x, x_before)
+        r.close()
+        bad_geom = dict(g, dso=5.0, dsd=9.0)
+        with pytest.raises(C.CtError) as e:
+            C.ct_geom_create(C.geom_desc(bad_geom))
+        assert e.value.status == C.CT_E_CONFIG
+        # empty view descriptor is a no-op
+        C.ct_forward(h, x, C.views(0, 1, 0), p)
+        assert float(p.min()) == 7.0
+    finally:
+        C.ct_geom_destroy(h)
+
+
+def test_deterministic_repeat(C):
+    pb = synthetic_problem(tiny("helical_arc"), M=3)
+    outs = []
+    for _ in range(2):
+        rec = _gpu_recon(pb)
+        rec.run(5)
+        outs.append(host(rec.x))
+        rec.close()
+    assert np.array_equal(outs[0], outs[1])
