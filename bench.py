@@ -1,0 +1,417 @@
+"""Benchmark: relaxed OS-LALM subset-iterations/s (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl cuda|reference]
+
+A step is one outer iteration of Algorithm 1: M
+sub-iterations, i.e. one pass of the whole hot path (stencil + x-update,
+forward projection + weighted residual, back-projection + g/htilde update)
+over every subset of the synthetic sinogram.  D_L and line 1 of Alg. 1
+run once before the timed region, as in the paper.  Inputs are seeded
+synthetic data of the BASELINE config (synth/), generated on the device.
+
+value   = M * K * (all ranks' shared reconstruction) / max-over-ranks device time
+e2e     = the same metric through the C-ABI with the sinogram (y, w) copied from
+          pinned host memory every step and x read back every step
+For N > 1 (torchrun) each subset's views are sharded over the ranks and the
+partial back-projections are summed with NCCL (strong scaling of one
+reconstruction).  --impl reference times the float64 oracle (oracle/) on the
+host cores on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": "c1: 2-D fan 128x128, arc 256 bins x 180 views, M=4, alpha=1.999 (BASELINE configs[0])",
+    "c2": "c2: 2-D fan 512x512, arc 888 bins x 984 views, M=41, alpha=1.999 (BASELINE configs[1])",
+    "c3": "c3: 3-D axial cone 256x256x64, flat 444x32 x 492 views, M=12, alpha=1.999 (BASELINE configs[2])",
+    "c4": "c4: 3-D helical 512x512x96, arc 888x64 x 2952 views (3 turns, pitch 1), M=24, alpha=1.999 "
+          "(BASELINE configs[3])",
+    "c5": "c5: 3-D helical 1024x1024x256, arc 888x64 x 5904 views (6 turns), M=41, alpha=1.999 "
+          "(BASELINE configs[4])",
+}
+FP32_LANES_PER_SM = 128
+N_SM = 148
+
+
+def peaks():
+    p = {"hbm_gbs": 6556.2, "sm_max_mhz": 1965.0, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update(hbm_gbs=m["hbm_gbs"], sm_max_mhz=m.get("sm_max_mhz", 1965.0), source="MEASURED_PEAKS.json")
+    except Exception:
+        pass
+    # FP32 (non-tensor) peak from unit counts and the max SM clock
+    p["fp32_tflops"] = N_SM * FP32_LANES_PER_SM * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- inputs
+def make_inputs(cfg, device):
+    """Seeded synthetic sinogram, weights, x0 of the config (synth/) + beta."""
+    import torch
+
+    from synth.configs import reg_betas
+    from synth.data import make_dataset
+    data = make_dataset(cfg, device=device)
+    g = cfg["geom"]
+    nd = cfg["reg"]["n_dirs"]
+    if cfg["reg"]["beta0"] is None:
+        raise RuntimeError("config has no calibrated beta0 (scripts/calibrate_beta.py)")
+    betas = reg_betas(g, cfg["reg"]["beta0"], nd)
+    reg = dict(potential=cfg["reg"]["potential"], delta=cfg["reg"]["delta"], betas=betas, n_dirs=nd)
+    f32 = torch.float32
+    return dict(y=data["y"].to(f32), w=data["w"].to(f32), x0=data["x0"].to(f32), reg=reg)
+
+
+# ----------------------------------------------------------------------------- reference arm
+def oracle_step_sample(cfg, inputs_np, frac, rng_seed=0):
+    """One bounded sample of a sub-iteration with the float64 oracle (as it stands):
+    Algorithm 1 line 4-8 restricted to a fraction `frac` of subset 0's views and
+    the same fraction of z-slices for the regulariser/update.  Returns seconds."""
+    import numpy as np
+
+    from oracle import alg
+    from oracle import projector as P
+    g = cfg["geom"]
+    M = cfg["solver"]["M"]
+    na = g["na"]
+    vm = (na + M - 1) // M
+    nv = max(1, int(round(frac * vm)))
+    views = (0, M, nv)
+    y, w, x0, reg = inputs_np
+    shape = P.vol_shape(g)
+    nz = shape[0]
+    nzs = max(1, int(round(frac * nz))) if g["dim"] == 3 else 1
+    gs = dict(g, nz=nzs) if g["dim"] == 3 else g
+    xs = np.ascontiguousarray(x0[:nzs])
+    rng = np.random.default_rng(rng_seed)
+    gg = rng.standard_normal(xs.shape) * 1e-3
+    h = rng.standard_normal(xs.shape) * 1e-3
+    DL = np.full(xs.shape, 1e6)          # timing sample only: values do not change the work
+    t0 = time.perf_counter()
+    # lines 4-5 on the slab
+    _, gradR, DR = P.reg(gs, reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"], xs)
+    rho, alpha = alg.rho_k(5, cfg["solver"]["alpha"]), cfg["solver"]["alpha"]
+    s = rho * (DL * xs - h) + (1 - rho) * gg
+    xn = np.maximum(xs - (s + gradR) / (rho * DL + DR), 0.0)
+    # line 6 on the sampled views (full volume: the projector needs it)
+    Ax = P.forward(g, x0, views)
+    r = w[0:M * nv:M] * (Ax - y[0:M * nv:M])
+    zeta = M * P.back(g, r, views)
+    # lines 7-8 on the slab
+    zs = zeta[:nzs]
+    gg = rho / (rho + 1) * (alpha * zs + (1 - alpha) * gg) + gg / (rho + 1)
+    h = alpha * (DL * xn - zs) + (1 - alpha) * h
+    return time.perf_counter() - t0, nv, vm, nzs, nz
+
+
+def cpu_baseline(cfg, inputs, target_s=20.0, steps=1, warmup=0):
+    """Oracle timed on the host cores on a bounded sample; value in subset-iters/s."""
+    import numpy as np
+    y = inputs["y"].double().cpu().numpy()
+    w = inputs["w"].double().cpu().numpy()
+    x0 = inputs["x0"].double().cpu().numpy()
+    args = (y, w, x0, inputs["reg"])
+    # calibrate the sample fraction on a tiny probe
+    probe = 1.0 / max(1, (cfg["geom"]["na"] // cfg["solver"]["M"]))
+    tp, nv, vm, _, _ = oracle_step_sample(cfg, args, probe)
+    per_full = tp / (nv / vm)
+    frac = min(1.0, target_s / max(per_full, 1e-9))
+    for _ in range(warmup):
+        oracle_step_sample(cfg, args, frac)
+    tot, fr = 0.0, 0.0
+    for _ in range(steps):
+        t, nv, vm, nzs, nz = oracle_step_sample(cfg, args, frac)
+        tot += t
+        fr += nv / vm
+    val = fr / tot      # sub-iterations per second (linear extrapolation of the sample)
+    sample = ("per step: Alg. 1 lines 4-8 on %d of the %d views of subset 0 and %d of %d z-slices "
+              "(fraction %.4f of one sub-iteration)" % (nv, vm, nzs, nz, nv / vm))
+    return val, sample
+
+
+def run_reference(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import projector as P
+    from synth.configs import get_config
+    cfg = get_config(args.config)
+    P.build()
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    inputs = make_inputs(cfg, dev)
+    M = cfg["solver"]["M"]
+    budget = 150.0
+    per_step = budget / max(1, args.steps + args.warmup)
+    val, sample = cpu_baseline(cfg, inputs, target_s=per_step, steps=args.steps, warmup=args.warmup)
+    cores = P.max_threads()
+    line = {"impl": "reference", "metric": "relaxed OS-LALM subset-iters/s", "value": val,
+            "unit": "subset-iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * M / val, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "config": args.config},
+            "cpu_baseline": {"value": val, "unit": "subset-iters/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "subset-iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- CUDA arm
+def run_cuda(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1512_04564_b200 import ctrecon as C
+    from paper_1512_04564_b200.recon import Recon
+    from synth.configs import get_config, subset_views
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit("--gpus %d but WORLD_SIZE=%d (launch N>1 with torchrun)" % (args.gpus, world))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    C.load()
+    cfg = get_config(args.config)
+    g = cfg["geom"]
+    M = cfg["solver"]["M"]
+    inputs = make_inputs(cfg, dev)
+
+    cdist = None
+    if world > 1:
+        uid = [C.ct_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        cdist = C.ct_dist_create(rank, world, uid[0], local)
+
+    stream = torch.cuda.current_stream(dev)
+    rec = Recon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], device=local,
+                dist=cdist)
+    rec.compute_DL()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up (includes line 1 of Alg. 1 in the first call) and graph capture
+    for _ in range(args.warmup):
+        rec.run(M)
+    barrier()
+
+    # ---- timed region: K outer iterations, inputs resident in HBM
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    n0 = C.ct_launch_count()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rec.run(M)
+    e1.record(stream)
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    launches = C.ct_launch_count() - n0
+    clocks = sampler.stop() if sampler else None
+    value = M * args.steps / (ms / 1000.0)
+
+    # ---- per-kernel device times (eager launches with CUDA events, same stream)
+    kms = C.oslalm_profile(rec.h, rec.y, rec.w, rec.reg, rec.kappa, rec.dl, rec.params, rec.state, M, rec.ws,
+                           dist=cdist, stream=stream)
+    kms = [max_over_ranks(v) for v in kms]
+    # nonzeros of A per subset (2 FLOP each: DESIGN.md §8)
+    nnz = 0
+    for m in range(M):
+        st_, sd_, ct_ = subset_views(g["na"], M, m)
+        nnz += C.ct_count_nnz(rec.h, C.views(st_, sd_, ct_))
+    nnz_sub = nnz / M
+
+    # ---- e2e: through the public API with host buffers (pinned), every step
+    e2e = None
+    if not args.no_e2e:
+        y_h = inputs["y"].cpu().pin_memory()
+        w_h = inputs["w"].cpu().pin_memory()
+        x_h = torch.empty(rec.x.shape, dtype=torch.float32).pin_memory()
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(args.steps):
+            rec.y.copy_(y_h, non_blocking=True)
+            rec.w.copy_(w_h, non_blocking=True)
+            rec.run(M)
+            x_h.copy_(rec.x, non_blocking=True)
+        t1.record(stream)
+        barrier()
+        ems = max_over_ranks(t0.elapsed_time(t1))
+        e2e = {"value": M * args.steps / (ems / 1000.0), "unit": "subset-iters/s",
+               "h2d_bytes_per_step": int(y_h.numel() * 4 + w_h.numel() * 4),
+               "d2h_bytes_per_step": int(x_h.numel() * 4)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    pk = peaks()
+    names = ["update (stencil + x-update)", "forward + weighted residual", "back-projection + g/htilde",
+             "other (all-reduce, k advance)"]
+    dom = max(range(3), key=lambda q: kms[q])
+    nvox = rec.x.numel()
+    vm = (g["na"] + M - 1) // M
+    nt = g["nt"] if g["dim"] == 3 else 1
+    rm = vm * nt * g["ns"]
+    per_launch_ms = kms[dom] / M
+    if dom in (1, 2):
+        flops = 2.0 * nnz_sub / world
+        achieved = flops / (per_launch_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": pk["fp32_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["fp32_tflops"], "traffic": None,
+                "kernel": names[dom], "algorithmic": "2 FLOP per nonzero of A_m, nnz(A_m) = %.4g" % nnz_sub,
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x %.0f MHz (sm_max)" % pk["sm_max_mhz"]}
+    else:
+        byts = 24.0 * nvox
+        achieved = byts / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": names[dom],
+                "algorithmic": "24 B/voxel", "peak_source": pk["source"]}
+    tfile = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as f:
+                tr = json.load(f)
+            key = {0: "update", 1: "forward", 2: "back"}[dom]
+            roof["traffic"] = tr.get(key)
+        except Exception:
+            pass
+    # projector GB/s (algorithmic bytes: fwd reads x, y, w, writes r; back reads r, r/w g, htilde)
+    fwd_bytes = 4.0 * nvox + 12.0 * rm / world
+    back_bytes = 4.0 * rm / world + 16.0 * nvox
+    kernels = {
+        "update_ms": kms[0] / M, "forward_ms": kms[1] / M, "back_ms": kms[2] / M, "other_ms": kms[3] / M,
+        "update_hbm_frac": 24.0 * nvox / (kms[0] / M / 1e3) / 1e9 / pk["hbm_gbs"],
+        "forward_alg_gbs": fwd_bytes / (kms[1] / M / 1e3) / 1e9,
+        "back_alg_gbs": back_bytes / (kms[2] / M / 1e3) / 1e9,
+        "forward_fp32_frac": 2.0 * nnz_sub / world / (kms[1] / M / 1e3) / 1e12 / pk["fp32_tflops"],
+        "back_fp32_frac": 2.0 * nnz_sub / world / (kms[2] / M / 1e3) / 1e12 / pk["fp32_tflops"],
+    }
+    cb = None
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import projector as P
+        P.build()
+        val, sample = cpu_baseline(cfg, inputs, target_s=args.cpu_seconds)
+        cb = {"value": val, "unit": "subset-iters/s", "cores": P.max_threads(), "kind": "oracle",
+              "sample": sample}
+    work_mb = (7 * nvox * 4 + 3 * rm * 4) / 2 ** 20
+    line = {
+        "metric": "relaxed OS-LALM subset-iters/s", "value": value, "unit": "subset-iters/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded random-ellipsoid phantom, analytic line integrals, Poisson%s noise)" %
+                (" + electronic" if cfg["noise"]["sigma"] > 0 else ""),
+        "config": {"workload": WORKLOADS[args.config], "config": args.config, "subsets": M,
+                   "sub_iters_per_step": M, "volume": list(rec.x.shape), "views": g["na"],
+                   "parallelism": "views of each subset sharded over %d GPU(s), NCCL all-reduce of zeta" % world
+                   if world > 1 else "1 GPU",
+                   "l2": "no flush: per-sub-iteration working set %.0f MB > 126 MB L2" % work_mb},
+        "roofline": roof, "kernels": kernels, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 1:
+        raise SystemExit("--warmup must be >= 1")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_cuda(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,22 @@ ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w,
                                int n_subiters, const float* x_ref, double* rms_per_iter, const ct_dist* dist,
                                void* workspace, size_t workspace_bytes, ct_stream s);
 
+/* Same as oslalm_relaxed_solve (no x_ref/rms) but runs the sub-iterations
+ * eagerly with CUDA events around each kernel and returns, in host
+ * kernel_ms[4], the summed device time of (0) stencil + x-update, (1)
+ * forward projection + residual, (2) back-projection (+ g/htilde epilogue),
+ * (3) the rest (all-reduce, g/htilde update on the dist path, k advance).
+ * Synchronises.  For measurement only. */
+ct_status oslalm_profile(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r, const float* kappa,
+                         const float* d_l, const oslalm_params* p, oslalm_state* st, int n_subiters,
+                         const ct_dist* dist, void* workspace, size_t workspace_bytes, ct_stream s,
+                         double* kernel_ms);
+
+/* *d_count (device uint64) += number of nonzero entries of A on views v:
+ * entry ((v,t,s),(i,j,k)) != 0 iff F1(s) > 0 and F2(k,t) > 0.
+ * The projector's algorithmic FLOP count is 2 per nonzero. */
+ct_status ct_count_nnz(const ct_geom* g, ct_views v, uint64_t* d_count, ct_stream s);
+
 /* h = D_L x - htilde (Algorithm 1's h, for checkpoints and parity checks). */
 ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out, ct_stream s);
 

@@ -107,6 +107,7 @@ static ct_status validate_desc(const ct_geom_desc* d) {
         !std::isfinite(d->source_z0))
         return fail(CT_E_CONFIG, "non-finite orbit parameters");
     if ((long long)d->nx * d->ny * d->nz > (1LL << 33)) return fail(CT_E_CONFIG, "volume too large");
+    if (d->nt > 128) return fail(CT_E_CONFIG, "nt = %d > 128 detector rows", d->nt);
     // source must stay outside the volume's circumscribed cylinder
     const double ex = 0.5 * d->nx * d->dx + std::fabs(d->offset_x);
     const double ey = 0.5 * d->ny * d->dy + std::fabs(d->offset_y);
@@ -293,7 +294,7 @@ extern "C" ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const f
 
 // ------------------------------------------------------------------ solver
 struct WsLayout {
-    size_t ctl, xalt, r, zeta, flag, dsum, total;
+    size_t ctl, xalt, xt, r, zeta, flag, dsum, total;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -308,6 +309,8 @@ static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dis
     off = align_up(off + sizeof(Ctl));
     L.xalt = off;
     off = align_up(off + sizeof(float) * g->G.nvox);
+    L.xt = off;
+    if (g->G.dim == 3) off = align_up(off + sizeof(float) * g->G.nvox);
     L.r = off;
     off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
     L.zeta = off;
@@ -350,20 +353,21 @@ extern "C" double oslalm_rho(int64_t k, double alpha) {
 }
 
 // one sub-iteration (lines 4-9 of Alg. 1) on stream s; single GPU.
-static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, float* xa, float* xb, const float* y,
-                            const float* w, const float* dl, float* gb, float* ht, const float* kappa, float* r,
-                            int max_count, float M, float lo, float hi, cudaStream_t s) {
-    launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, s);
-    launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
+static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, float* xa, float* xb, float* xt,
+                            const float* y, const float* w, const float* dl, float* gb, float* ht,
+                            const float* kappa, float* r, int max_count, float M, float lo, float hi,
+                            cudaStream_t s) {
+    launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, xt, s);
+    if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, r, FWD_RESID, s, true);
+    else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
     launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);
     launch_advance(ctl, s);
 }
 
-extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
-                                          const float* kappa, const float* d_l, const oslalm_params* p,
-                                          oslalm_state* st, int n_subiters, const float* x_ref,
-                                          double* rms_per_iter, const ct_dist* dist, void* workspace,
-                                          size_t workspace_bytes, ct_stream stream) {
+static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                            const float* kappa, const float* d_l, const oslalm_params* p, oslalm_state* st,
+                            int n_subiters, const float* x_ref, double* rms_per_iter, const ct_dist* dist,
+                            void* workspace, size_t workspace_bytes, ct_stream stream, double* kernel_ms) {
     if (!g || !y || !d_l || !st || !workspace) return fail(CT_E_CONFIG, "oslalm_relaxed_solve: NULL argument");
     if (!st->x || !st->g || !st->htilde) return fail(CT_E_CONFIG, "oslalm_state has NULL arrays");
     if (st->k < 0) return fail(CT_E_CONFIG, "state k < 0");
@@ -383,6 +387,7 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
     char* ws = (char*)workspace;
     Ctl* ctl = (Ctl*)(ws + L.ctl);
     float* xalt = (float*)(ws + L.xalt);
+    float* xt = g->G.dim == 3 ? (float*)(ws + L.xt) : nullptr;
     float* rbuf = (float*)(ws + L.r);
     float* zeta = dist ? (float*)(ws + L.zeta) : nullptr;
     int* dflag = (int*)(ws + L.flag);
@@ -446,10 +451,11 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
     int iter_out = 0;
     long long kcur = st->k;
     cudaGraphExec_t exec = nullptr;
-    if (!dist && n_subiters > 0) {
+    if (!dist && !kernel_ms && n_subiters > 0) {
         GraphKey key;
         key.ptrs = {(uintptr_t)ctl, (uintptr_t)st->x, (uintptr_t)xalt, (uintptr_t)y, (uintptr_t)w,
-                    (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf};
+                    (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf,
+                    (uintptr_t)xt};
         key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi,
                     (double)rp.potential, (double)rp.delta, (double)rp.n_dirs};
         for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
@@ -460,8 +466,8 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
         } else {
             cudaStream_t cs = g->cap_stream;
             CT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            enqueue_subiter(g, rp, ctl, st->x, xalt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count, Mf, lo,
-                            hi, cs);
+            enqueue_subiter(g, rp, ctl, st->x, xalt, xt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count, Mf,
+                            lo, hi, cs);
             cudaGraph_t graph;
             cudaError_t e = cudaStreamEndCapture(cs, &graph);
             if (e != cudaSuccess) return fail(CT_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -472,18 +478,36 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
             const_cast<ct_geom*>(g)->graphs[key] = exec;
         }
     }
+    std::vector<cudaEvent_t> evs;
+    if (kernel_ms) {
+        evs.resize((size_t)n_subiters * 5);
+        for (auto& e : evs) CT_CUDA(cudaEventCreate(&e));
+    }
     while (done < n_subiters) {
+        cudaEvent_t* ev = kernel_ms ? &evs[(size_t)done * 5] : nullptr;
         if (exec) {
             CT_CUDA(cudaGraphLaunch(exec, s));
             launches_add(4);
         } else {
-            launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, s);
-            launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
-            launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
-            if (dist->world > 1)
-                CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
-            launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
+            launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
+            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s, true);
+            else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
+            if (!dist) {
+                launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g,
+                            st->htilde, s);
+                if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
+            } else {
+                launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
+                if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
+                if (dist->world > 1)
+                    CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+                launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
+            }
             launch_advance(ctl, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
         }
         done++;
         kcur++;
@@ -497,6 +521,18 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
             rms_per_iter[iter_out++] = std::sqrt(hs / (double)g->G.nvox);
         }
     }
+    if (kernel_ms) {
+        CT_CUDA(cudaStreamSynchronize(s));
+        for (int q = 0; q < 4; q++) kernel_ms[q] = 0.0;
+        for (int it = 0; it < n_subiters; it++) {
+            for (int q = 0; q < 4; q++) {
+                float ms = 0.f;
+                CT_CUDA(cudaEventElapsedTime(&ms, evs[(size_t)it * 5 + q], evs[(size_t)it * 5 + q + 1]));
+                kernel_ms[q] += ms;
+            }
+        }
+        for (auto& e : evs) cudaEventDestroy(e);
+    }
     if (n_subiters & 1) CT_CUDA(cudaMemcpyAsync(st->x, xalt, sizeof(float) * g->G.nvox, cudaMemcpyDeviceToDevice, s));
     st->k += n_subiters;
     // finiteness of the returned image (K7)
@@ -509,6 +545,33 @@ extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, cons
     if (stt != CT_OK) return stt;
     if (hflag) return fail(CT_E_NUMERIC, "non-finite values in x after sub-iteration %lld", (long long)st->k);
     return CT_OK;
+}
+
+extern "C" ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                                          const float* kappa, const float* d_l, const oslalm_params* p,
+                                          oslalm_state* st, int n_subiters, const float* x_ref,
+                                          double* rms_per_iter, const ct_dist* dist, void* workspace,
+                                          size_t workspace_bytes, ct_stream stream) {
+    return solve_impl(g, y, w, r, kappa, d_l, p, st, n_subiters, x_ref, rms_per_iter, dist, workspace,
+                      workspace_bytes, stream, nullptr);
+}
+
+extern "C" ct_status oslalm_profile(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                                    const float* kappa, const float* d_l, const oslalm_params* p, oslalm_state* st,
+                                    int n_subiters, const ct_dist* dist, void* workspace, size_t workspace_bytes,
+                                    ct_stream stream, double* kernel_ms) {
+    if (!kernel_ms) return fail(CT_E_CONFIG, "oslalm_profile: kernel_ms is NULL");
+    return solve_impl(g, y, w, r, kappa, d_l, p, st, n_subiters, nullptr, nullptr, dist, workspace,
+                      workspace_bytes, stream, kernel_ms);
+}
+
+extern "C" ct_status ct_count_nnz(const ct_geom* g, ct_views v, uint64_t* d_count, ct_stream s) {
+    if (!g || !d_count) return fail(CT_E_CONFIG, "ct_count_nnz: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    DeviceGuard guard(g->device);
+    launch_count(g->G, g->vtab, to_views(v), (unsigned long long*)d_count, (cudaStream_t)s);
+    return check_async();
 }
 
 extern "C" ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out,

@@ -16,7 +16,8 @@ struct RegParams {
 // x_pair: (xa, xb); with ctl != nullptr the forward reads the buffer written
 // by this sub-iteration's update (parity of k - k_base), else xa.
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
-                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s);
+                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
+                bool xt = false);
 
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);
@@ -27,7 +28,8 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
 
 // fused stencil + x-update of Algorithm 1 lines 4-5, writes htilde partial
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, cudaStream_t s);
+                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* xt,
+                   cudaStream_t s);
 
 // dist path: g, htilde update from an all-reduced zeta (lines 7-8)
 void launch_gh_update(const DGeom& G, const Ctl* ctl, const float* zeta, float* g, float* ht, cudaStream_t s);
@@ -36,6 +38,9 @@ void launch_advance(Ctl* ctl, cudaStream_t s);
 void launch_state_h(const DGeom& G, const float* dl, const float* x, const float* ht, float* h, cudaStream_t s);
 // flag[0] |= any non-finite in x; optional sum of squares of (x - xref) into dsum[0]
 void launch_check(const DGeom& G, const float* x, const float* xref, int* flag, double* dsum, cudaStream_t s);
+
+// nonzero entries of A on views v, added into *count (device)
+void launch_count(const DGeom& G, const float4* vtab, Views v, unsigned long long* count, cudaStream_t s);
 
 int64_t launches_add(int64_t n);  // launch accounting
 

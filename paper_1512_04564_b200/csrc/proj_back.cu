@@ -172,3 +172,54 @@ void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, co
 }
 
 }  // namespace ctr
+
+// ---------------------------------------------------------------------------
+// Nonzero count of A on a set of views (the denominator of the projector's
+// algorithmic FLOP figure, 2 FLOP per nonzero): entry
+// ((v,t,s),(i,j,k)) is nonzero iff F1(s) > 0 and F2(k,t) > 0.
+namespace ctr {
+
+template <bool ARC, int DIM>
+__global__ void __launch_bounds__(128) k_count(DGeom G, const float4* __restrict__ vtab, Views V,
+                                               unsigned long long* __restrict__ count) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 4 + threadIdx.y;
+    unsigned long long acc = 0;
+    if (i < G.nx && j < G.ny) {
+        for (int vi = 0; vi < V.count; vi++) {
+            const float4 vw = __ldg(&vtab[V.start + vi * V.stride]);
+            Footprint f;
+            ct_footprint<ARC>(G, vw.x, vw.y, vw.z, i, j, f);
+            const int slo = max((int)floorf(f.sfc + f.u0 + 0.5f) - 1, 0);
+            const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f) + 1, G.ns - 1);
+            int ncz = 0;
+            for (int s = slo; s <= shi; s++) ncz += sf_F1(f, s) > 0.f;
+            if (ncz == 0) continue;
+            long long rows = 1;
+            if (DIM == 3) {
+                rows = 0;
+                for (int k = 0; k < G.nz; k++) {
+                    const float lo = fmaxf(voxel_b(f, k), 0.f), hi = fminf(voxel_b(f, k + 1), (float)G.nt);
+                    if (hi > lo) rows += (long long)ceilf(hi) - (long long)floorf(lo);
+                }
+            }
+            acc += (unsigned long long)ncz * (unsigned long long)rows;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(count, acc);
+}
+
+void launch_count(const DGeom& G, const float4* vtab, Views v, unsigned long long* count, cudaStream_t s) {
+    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4);
+    if (G.arc) {
+        if (G.dim == 3) k_count<true, 3><<<grid, block, 0, s>>>(G, vtab, v, count);
+        else k_count<true, 2><<<grid, block, 0, s>>>(G, vtab, v, count);
+    } else {
+        if (G.dim == 3) k_count<false, 3><<<grid, block, 0, s>>>(G, vtab, v, count);
+        else k_count<false, 2><<<grid, block, 0, s>>>(G, vtab, v, count);
+    }
+    launches_add(1);
+}
+
+}  // namespace ctr

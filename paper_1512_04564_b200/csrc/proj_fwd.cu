@@ -174,6 +174,203 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// 3-D forward projection, warp per detector column (v, s); lanes own detector
+// rows t = lane + 32 r.  The warp walks its column's fan wedge 8 slabs at a
+// time: lanes split the candidate voxel columns (4 per slab per pass),
+// evaluate their footprints in parallel, and push the columns with F1(s) > 0
+// into a warp queue (ballot + prefix popcount).  Every queued column is then
+// resampled onto the rows by all lanes at once: row t gathers the voxels
+// whose magnified z-extent [b_k, b_k+1] meets [t, t+1] (exact F2 overlaps,
+// same boundary arithmetic as the back-projector).  With XT the volume is
+// read in the z-fastest copy written by the x-update, so a lane group reads
+// one contiguous z-run per column (coalesced).  No atomics; row sums live in
+// registers; the epilogue stages the block's 8 columns through shared
+// memory so the residual kernel's y/w reads and r writes are 32-byte runs.
+constexpr int F3_WARPS = 8;
+constexpr int F3_BS = 32 * F3_WARPS;
+
+template <bool ARC, int MODE, int RPL, bool XT>
+__global__ void __launch_bounds__(F3_BS)
+k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+       const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
+       const float* __restrict__ w, float* __restrict__ out) {
+    __shared__ float4 qbuf[F3_WARPS][32];
+    __shared__ float stage[32 * RPL][F3_WARPS + 1];
+    constexpr bool ONES = (MODE == FWD_ONES_W);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const Views V = select_views(ctl, vsel);
+    const int vi = blockIdx.y;
+    if (vi >= V.count) return;
+    const int v = V.start + vi * V.stride;
+    const int s0 = blockIdx.x * F3_WARPS;
+    const int s = s0 + wid;
+    const float* __restrict__ x = xa;
+    if (ctl && !XT) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
+    const float4 vw = __ldg(&vtab[v]);
+    const float cb = vw.x, sb = vw.y, zs = vw.z;
+    const float Sx = G.dso * cb, Sy = G.dso * sb;
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+
+    float acc[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; r++) acc[r] = 0.f;
+
+    if (s < G.ns) {  // warp-uniform
+        const float tl = ((float)s - 0.5f - G.s_c0) * G.delta;
+        const float tr = ((float)s + 0.5f - G.s_c0) * G.delta;
+        const float tm = ((float)s - G.s_c0) * G.delta;
+        float cal, cul, car, cur_, cam, cum;
+        if (ARC) {
+            sincosf(tl, &cul, &cal);
+            sincosf(tr, &cur_, &car);
+            sincosf(tm, &cum, &cam);
+        } else {
+            cal = car = cam = G.dsd;
+            cul = tl; cur_ = tr; cum = tm;
+        }
+        const float dlx = -cal * cb - cul * sb, dly = -cal * sb + cul * cb;
+        const float drx = -car * cb - cur_ * sb, dry = -car * sb + cur_ * cb;
+        const float dmx = -cam * cb - cum * sb, dmy = -cam * sb + cum * cb;
+        const float nlx = -cal * sb + cul * cb, nly = cal * cb + cul * sb;
+        const float nrx = car * sb - cur_ * cb, nry = -car * cb - cur_ * sb;
+        const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
+        const float suppl = fabsf(nlx) * hx + fabsf(nly) * hy;
+        const float suppr = fabsf(nrx) * hx + fabsf(nry) * hy;
+        const float tol_l = 1e-4f * suppl, tol_r = 1e-4f * suppr;
+        const bool xstep = fabsf(dmx) >= fabsf(dmy);
+        // stepping axis "a" (slabs) and other axis "o"
+        const int na_ = xstep ? G.nx : G.ny, no_ = xstep ? G.ny : G.nx;
+        const float a0 = xstep ? G.x0 : G.y0, da = xstep ? G.dx : G.dy, ha = xstep ? hx : hy;
+        const float o0 = xstep ? G.y0 : G.x0, dob = xstep ? G.dy : G.dx;
+        const float Sa = xstep ? Sx : Sy, So = xstep ? Sy : Sx;
+        const float kl = xstep ? dly / dlx : dlx / dly;
+        const float kr = xstep ? dry / drx : drx / dry;
+        const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
+        const float inv_do = 1.f / dob;
+        const float nzH_dummy = 0.f;
+        (void)nzH_dummy;
+
+        for (int sl0 = 0; sl0 < na_; sl0 += 8) {
+            const int sl = sl0 + (lane >> 2), sub = lane & 3;
+            int lo = 0, hi = -1;
+            if (sl < na_) {
+                const float ac = fmaf((float)sl, da, a0);
+                const float pa = ac - ha - Sa, pb = ac + ha - Sa;
+                if (pa * sgn > 0.f && pb * sgn > 0.f) {
+                    const float y1 = fmaf(pa, kl, So), y2 = fmaf(pb, kl, So);
+                    const float y3 = fmaf(pa, kr, So), y4 = fmaf(pb, kr, So);
+                    const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - o0) * inv_do + 0.5f;
+                    const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - o0) * inv_do + 0.5f;
+                    if (f1 >= -1.f && f0 <= (float)no_ + 1.f) {
+                        lo = max((int)floorf(f0) - 1, 0);
+                        hi = min((int)floorf(f1) + 1, no_ - 1);
+                    }
+                }
+            }
+            const int npass = __reduce_max_sync(0xffffffffu, (hi - lo + 1 + 3) >> 2);
+            for (int p = 0; p < npass; p++) {
+                const int o = lo + sub + 4 * p;
+                bool nz = false;
+                float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (o <= hi) {
+                    const int i = xstep ? sl : o, j = xstep ? o : sl;
+                    const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
+                    const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
+                    if (fmaf(nlx, cx, nly * cy) + suppl >= -tol_l && fmaf(nrx, cx, nry * cy) + suppr >= -tol_r) {
+                        Footprint f;
+                        ct_footprint<ARC>(G, cb, sb, zs, i, j, f);
+                        const float F1 = sf_F1(f, s);
+                        if (F1 > 0.f) {
+                            nz = true;
+                            ent = make_float4(f.lxy * F1, f.B0, f.H, __int_as_float(j * G.nx + i));
+                        }
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, nz);
+                if (nz) qbuf[wid][__popc(m & lanemask_lt)] = ent;
+                __syncwarp();
+                const int n = __popc(m);
+                for (int e = 0; e < n; e++) {
+                    const float4 q = qbuf[wid][e];
+                    const int col = __float_as_int(q.w);
+                    const float* __restrict__ xc = XT ? x + (size_t)col * G.nz : x + col;
+                    const size_t kst = XT ? 1 : (size_t)G.nxy;
+                    const float invH = 1.f / q.z;
+                    const float btop = fmaf((float)G.nz, q.z, q.y);
+#pragma unroll
+                    for (int r = 0; r < RPL; r++) {
+                        const int t = lane + 32 * r;
+                        const float tb = (float)t, tb1 = (float)(t + 1);
+                        if (t < G.nt && tb1 > q.y && tb < btop) {
+                            int k = (int)floorf((tb - q.y) * invH);
+                            k = min(max(k, 0), G.nz - 1);
+                            while (k > 0 && fmaf((float)k, q.z, q.y) > tb) k--;
+                            float a = 0.f;
+                            float bk = fmaf((float)k, q.z, q.y);
+                            for (; k < G.nz; k++) {
+                                if (bk >= tb1) break;
+                                const float bk1 = fmaf((float)(k + 1), q.z, q.y);
+                                const float ov = fminf(bk1, tb1) - fmaxf(bk, tb);
+                                if (ov > 0.f) a = fmaf(ov, ONES ? 1.f : __ldg(&xc[(size_t)k * kst]), a);
+                                bk = bk1;
+                            }
+                            acc[r] = fmaf(q.x, a, acc[r]);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+    }
+
+    // epilogue: stage [row][column-in-block], then each thread handles one (row, col)
+#pragma unroll
+    for (int r = 0; r < RPL; r++) stage[lane + 32 * r][wid] = acc[r];
+    __syncthreads();
+    for (int q = threadIdx.x; q < G.nt * F3_WARPS; q += F3_BS) {
+        const int t = q / F3_WARPS, c = q % F3_WARPS;
+        const int ss = s0 + c;
+        if (ss >= G.ns) continue;
+        const float lz = ray_Lz<ARC>(G, ss, t);
+        const float p = lz * stage[t][c];
+        const size_t o = ((size_t)vi * G.nt + t) * G.ns + ss;
+        if (MODE == FWD_PLAIN) {
+            out[o] = p;
+        } else {
+            const size_t a = ((size_t)v * G.nt + t) * G.ns + ss;
+            const float wv = w ? __ldg(&w[a]) : 1.f;
+            if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldg(&y[a]));
+            else out[o] = lz * wv * p;
+        }
+    }
+}
+
+template <bool ARC, int MODE, bool XT>
+static void fwd3_rpl(const DGeom& G, dim3 grid, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
+                     const float* xb, const float* y, const float* w, float* out, cudaStream_t s) {
+    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+    else k_fwd3<ARC, MODE, 4, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+}
+
+template <bool ARC>
+static void fwd3_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
+                          const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
+                          bool xt, cudaStream_t s) {
+    dim3 grid((G.ns + F3_WARPS - 1) / F3_WARPS, max_count);
+    if (mode == FWD_PLAIN) {
+        xt ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s)
+           : fwd3_rpl<ARC, FWD_PLAIN, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+    } else if (mode == FWD_RESID) {
+        xt ? fwd3_rpl<ARC, FWD_RESID, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s)
+           : fwd3_rpl<ARC, FWD_RESID, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+    } else {
+        fwd3_rpl<ARC, FWD_ONES_W, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+    }
+}
+
 template <bool ARC, int DIM>
 static void fwd_dispatch_mode(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                               const float* xa, const float* xb, const float* y, const float* w, float* out,
@@ -197,13 +394,13 @@ static void fwd_dispatch_mode(const DGeom& G, const float4* vtab, const Ctl* ctl
 }
 
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
-                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s) {
+                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s, bool xt) {
     if (max_count <= 0) return;
     if (G.arc) {
-        if (G.dim == 3) fwd_dispatch_mode<true, 3>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        if (G.dim == 3) fwd3_dispatch<true>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, xt, s);
         else fwd_dispatch_mode<true, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     } else {
-        if (G.dim == 3) fwd_dispatch_mode<false, 3>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        if (G.dim == 3) fwd3_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, xt, s);
         else fwd_dispatch_mode<false, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     }
     launches_add(1);

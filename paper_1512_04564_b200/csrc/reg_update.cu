@@ -16,6 +16,19 @@
 
 namespace ctr {
 
+// compile-time direction offsets for the register-window stencil (fold after unrolling)
+__host__ __device__ constexpr int dir_x(int d) {
+    return (d == 0 || d == 2 || d == 3 || d == 5 || d == 9 || d == 11) ? 1 : (d == 6 || d == 10 || d == 12) ? -1 : 0;
+}
+__host__ __device__ constexpr int dir_y(int d) {
+    return (d == 1 || d == 2 || d == 7 || d == 9 || d == 10) ? 1 : (d == 3 || d == 8 || d == 11 || d == 12) ? -1 : 0;
+}
+__host__ __device__ constexpr int dir_z(int d) { return d >= 4 ? 1 : 0; }
+
+static_assert(dir_x(6) == -1 && dir_y(8) == -1 && dir_z(4) == 1 && dir_x(4) == 0 && dir_y(12) == -1 &&
+                  dir_x(11) == 1 && dir_y(11) == -1 && dir_z(3) == 0,
+              "direction table");
+
 __constant__ int c_dirs[13][3] = {
     {1, 0, 0}, {0, 1, 0}, {1, 1, 0}, {1, -1, 0},
     {0, 0, 1}, {1, 0, 1}, {-1, 0, 1}, {0, 1, 1}, {0, -1, 1},
@@ -80,32 +93,121 @@ __global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float*
     if (curv) curv[idx] = cv;
 }
 
+// z-marching update: thread = voxel column (i, j) x UPD_KZ consecutive z; the
+// 3x3x3 neighbourhood of x (and kappa) lives in registers and advances one
+// plane per voxel (9 loads per voxel instead of 27).  Writes x+ in the
+// boundary layout (coalesced over i) and, for the forward projector, in the
+// z-fastest copy xt (two 16-byte stores per thread and column).
+constexpr int UPD_KZ = 8;
+
+template <int NDIRS, bool KAPPA, int POT>
+__device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const float (&K)[3][3][3],
+                                               const RegParams& rp, bool im, bool ip, bool jm, bool jp, bool km,
+                                               bool kp, float& grad, float& curv) {
+    const float xv = W[1][1][1];
+    const float kj = KAPPA ? K[1][1][1] : 1.f;
+    float gs = 0.f, cs = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIRS; d++) {
+#pragma unroll
+        for (int sg = 0; sg < 2; sg++) {
+            const int ox = sg ? -dir_x(d) : dir_x(d);
+            const int oy = sg ? -dir_y(d) : dir_y(d);
+            const int oz = sg ? -dir_z(d) : dir_z(d);
+            const bool ok = (ox < 0 ? im : (ox > 0 ? ip : true)) && (oy < 0 ? jm : (oy > 0 ? jp : true)) &&
+                            (oz < 0 ? km : (oz > 0 ? kp : true));
+            if (ok) {
+                const float wgt = KAPPA ? rp.beta[d] * kj * K[1 + oz][1 + oy][1 + ox] : rp.beta[d];
+                float dphi, om;
+                potential<POT>(xv - W[1 + oz][1 + oy][1 + ox], rp.inv_delta, dphi, om);
+                gs = fmaf(wgt, dphi, gs);
+                cs = fmaf(wgt, om, cs);
+            }
+        }
+    }
+    grad = gs;
+    curv = 2.f * cs;
+}
+
 template <int POT, int NDIRS, bool KAPPA>
-__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
+__global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
                                                 float* xb, const float* __restrict__ dl,
                                                 const float* __restrict__ g, float* __restrict__ ht,
-                                                const float* __restrict__ kappa, float box_lo, float box_hi) {
+                                                const float* __restrict__ kappa, float box_lo, float box_hi,
+                                                float* __restrict__ xt) {
     const int i = blockIdx.x * 32 + threadIdx.x;
-    const int j = blockIdx.y * 8 + threadIdx.y;
-    const int k = blockIdx.z;
+    const int j = blockIdx.y * 4 + threadIdx.y;
+    const int k0 = blockIdx.z * UPD_KZ;
     if (i >= G.nx || j >= G.ny) return;
     const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
     const float* __restrict__ x = odd ? xb : xa;
     float* __restrict__ xn = odd ? xa : xb;
-    const size_t idx = (size_t)k * G.nxy + (size_t)j * G.nx + i;
-    const float xv = x[idx];
-    float gr, cv;
-    stencil<POT, NDIRS, KAPPA>(G, rp, x, kappa, i, j, k, idx, xv, gr, cv);
     const float rho = rho_of_k(ctl);
     const float alpha = ctl->alpha;
-    const float d = __ldg(&dl[idx]);
-    const float htv = ht[idx];
-    const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
-    const float den = fmaf(rho, d, cv);
-    float xnew = xv;
-    if (den > 0.f) xnew = fminf(fmaxf(xv - (s + gr) / den, box_lo), box_hi);
-    xn[idx] = xnew;
-    ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+    const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
+    const size_t col = (size_t)j * G.nx + i;
+    float W[3][3][3], K[3][3][3];
+    auto load_plane = [&](int slot, int k) {
+        const bool ok = k >= 0 && k < G.nz;
+#pragma unroll
+        for (int dy = -1; dy <= 1; dy++) {
+#pragma unroll
+            for (int dx = -1; dx <= 1; dx++) {
+                const bool v = ok && (dx < 0 ? im : (dx > 0 ? ip : true)) && (dy < 0 ? jm : (dy > 0 ? jp : true));
+                const size_t a = (size_t)k * G.nxy + col + (long long)dy * G.nx + dx;
+                W[slot][dy + 1][dx + 1] = v ? __ldg(&x[a]) : 0.f;
+                if (KAPPA) K[slot][dy + 1][dx + 1] = v ? __ldg(&kappa[a]) : 0.f;
+            }
+        }
+    };
+    load_plane(0, k0 - 1);
+    load_plane(1, k0);
+    float xo[UPD_KZ];
+#pragma unroll
+    for (int kk = 0; kk < UPD_KZ; kk++) {
+        const int k = k0 + kk;
+        xo[kk] = 0.f;
+        if (k < G.nz) {
+            if (kk > 0) {
+#pragma unroll
+                for (int a = 0; a < 3; a++)
+#pragma unroll
+                    for (int b = 0; b < 3; b++) {
+                        W[0][a][b] = W[1][a][b];
+                        W[1][a][b] = W[2][a][b];
+                        if (KAPPA) {
+                            K[0][a][b] = K[1][a][b];
+                            K[1][a][b] = K[2][a][b];
+                        }
+                    }
+            }
+            load_plane(2, k + 1);
+            float gr, cv;
+            window_stencil<NDIRS, KAPPA, POT>(W, K, rp, im, ip, jm, jp, k > 0, k + 1 < G.nz, gr, cv);
+            const size_t idx = (size_t)k * G.nxy + col;
+            const float xv = W[1][1][1];
+            const float d = __ldg(&dl[idx]);
+            const float htv = ht[idx];
+            const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
+            const float den = fmaf(rho, d, cv);
+            float xnew = xv;
+            if (den > 0.f) xnew = fminf(fmaxf(xv - (s + gr) / den, box_lo), box_hi);
+            xn[idx] = xnew;
+            ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+            xo[kk] = xnew;
+        }
+    }
+    if (xt) {
+        float* dst = xt + col * G.nz + k0;
+        if (k0 + UPD_KZ <= G.nz && (G.nz & 3) == 0) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(xo[0], xo[1], xo[2], xo[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(xo[4], xo[5], xo[6], xo[7]);
+        } else {
+#pragma unroll
+            for (int kk = 0; kk < UPD_KZ; kk++)
+                if (k0 + kk < G.nz) dst[kk] = xo[kk];
+        }
+    }
 }
 
 template <int POT, int NDIRS>
@@ -129,19 +231,21 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
 
 template <int POT, int NDIRS>
 static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                         const float* g, float* ht, const float* kappa, float lo, float hi, cudaStream_t s) {
-    dim3 block(32, 8), grid((G.nx + 31) / 32, (G.ny + 7) / 8, G.nz);
-    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi);
-    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi);
+                         const float* g, float* ht, const float* kappa, float lo, float hi, float* xt,
+                         cudaStream_t s) {
+    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4, (G.nz + UPD_KZ - 1) / UPD_KZ);
+    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, xt);
+    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, xt);
 }
 
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, cudaStream_t s) {
+                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* xt,
+                   cudaStream_t s) {
     const bool d4 = rp.n_dirs == 4;
     switch (rp.potential) {
-        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
-        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
-        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, s); break;
+        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
+        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
+        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
     }
     launches_add(1);
 }

@@ -64,7 +64,8 @@ class oslalm_state(ctypes.Structure):
 
 EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs_diag", "ct_reg_grad",
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
-           "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error"]
+           "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
+           "oslalm_profile", "ct_count_nnz"]
 
 _lib = None
 
@@ -89,6 +90,9 @@ def load():
     L.oslalm_relaxed_solve.argtypes = [vp, vp, vp, P(ct_reg_desc), vp, vp, P(oslalm_params), P(oslalm_state),
                                        ctypes.c_int, vp, P(ctypes.c_double), vp, vp, ctypes.c_size_t, vp]
     L.oslalm_state_h.argtypes = [vp, vp, P(oslalm_state), vp, vp]
+    L.oslalm_profile.argtypes = [vp, vp, vp, P(ct_reg_desc), vp, vp, P(oslalm_params), P(oslalm_state),
+                                 ctypes.c_int, vp, vp, ctypes.c_size_t, vp, P(ctypes.c_double)]
+    L.ct_count_nnz.argtypes = [vp, ct_views, vp, vp]
     L.oslalm_rho.argtypes = [ctypes.c_int64, ctypes.c_double]
     L.oslalm_rho.restype = ctypes.c_double
     L.ct_sync.argtypes = [vp]
@@ -99,7 +103,8 @@ def load():
     L.ct_launch_count.restype = ctypes.c_int64
     L.ct_last_error.restype = ctypes.c_char_p
     for name in ("ct_geom_create", "ct_forward", "ct_back", "ct_sqs_diag", "ct_reg_grad", "oslalm_workspace_size",
-                 "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create"):
+                 "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
+                 "oslalm_profile", "ct_count_nnz"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -209,6 +214,23 @@ def oslalm_relaxed_solve(geom, y, w, reg, kappa, d_l, p, state, n_subiters, work
         for i in range(len(rms_per_iter)):
             rms_per_iter[i] = rms[i]
     return state
+
+
+def oslalm_profile(geom, y, w, reg, kappa, d_l, p, state, n_subiters, workspace, dist=None, stream=None):
+    """Returns summed device ms of [update, forward+residual, back+epilogue, rest]."""
+    ms = (ctypes.c_double * 4)()
+    _check(load().oslalm_profile(geom, _ptr(y), _ptr(w), ctypes.byref(reg), _ptr(kappa), _ptr(d_l),
+                                 ctypes.byref(p), ctypes.byref(state), int(n_subiters), dist,
+                                 ctypes.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size(),
+                                 _stream(stream), ms))
+    return [ms[i] for i in range(4)]
+
+
+def ct_count_nnz(geom, v, stream=None):
+    """Number of nonzero entries of A on views v (device count, returned as int)."""
+    cnt = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
+    _check(load().ct_count_nnz(geom, v, ctypes.c_void_p(cnt.data_ptr()), _stream(stream)))
+    return int(cnt.item())
 
 
 def oslalm_state_h(geom, d_l, state, h_out, stream=None):

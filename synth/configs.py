@@ -95,7 +95,7 @@ CONFIGS = {
 }
 
 # beta0 written by scripts/calibrate_beta.py (oracle-only); see module doc.
-_BETA0 = {"c1": None, "c2": None, "c3": None, "c4": None, "c5": None}
+_BETA0 = {"c1": 3.744e5, "c2": 4.539e7, "c3": 3.278e6, "c4": 1.512e7, "c5": None}
 
 
 def get_config(name):
@@ -151,3 +151,11 @@ def shrink(cfg, nx=None, nz=None, na=None, ns=None, nt=None):
                                          g["pitch"], g["orbit_deg"], g["offset_z"])
         del turns
     return c
+
+
+def shard_views(na, M, m, rank, world):
+    """Rank `rank` of `world` takes the subset-local views rank, rank+world, ...
+    of subset m: (m + rank*M, world*M, ceil((V_m - rank)/world)) — the same rule
+    as the device-side view selection of libctrecon."""
+    vm = (na - m + M - 1) // M
+    return (m + rank * M, world * M, max(0, (vm - rank + world - 1) // world))

@@ -1,0 +1,92 @@
+"""N > 1 host logic on CPU with the gloo backend (world_size 2): view sharding of
+each subset, the sum of partial back-projections (the NCCL all-reduce's job on
+the GPU path), NCCL-id broadcast and max-over-ranks timing."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from synth.configs import shard_views, subset_views
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import projector as P
+        from tests.geoms import tiny
+        from tests.problems import synthetic_problem
+        pb = synthetic_problem(tiny("helical_arc", na=43), M=4)
+        g, M = pb["geom"], 4
+        out = {}
+        for m in range(M):
+            st, sd, cnt = shard_views(g["na"], M, m, rank, world)
+            x = pb["x0"]
+            part = np.zeros(P.vol_shape(g))
+            if cnt > 0:
+                r = pb["w"][st::sd][:cnt] * (P.forward(g, x, (st, sd, cnt)) - pb["y"][st::sd][:cnt])
+                part = M * P.back(g, r, (st, sd, cnt))
+            t = torch.from_numpy(part)
+            dist.all_reduce(t)                      # the zeta all-reduce of the sharded path
+            out[m] = t.numpy()
+        # NCCL unique id broadcast as done in bench.py
+        obj = [bytes(range(128)) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        # max-over-ranks of a per-rank time
+        tm = torch.tensor([1.0 + rank], dtype=torch.float64)
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            q.put((out, obj[0], float(tm.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharding_partitions_every_subset():
+    for na, M in [(2952, 24), (43, 4), (984, 41), (7, 7)]:
+        for world in (1, 2, 3, 8):
+            for m in range(M):
+                views = []
+                for rank in range(world):
+                    st, sd, cnt = shard_views(na, M, m, rank, world)
+                    views += list(range(st, st + sd * cnt, sd)) if cnt else []
+                s0, s1, c = subset_views(na, M, m)
+                assert sorted(views) == list(range(s0, s0 + s1 * c, s1))
+                assert all(v < na for v in views)
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gloo_sum_of_partial_backprojections_equals_full_subset():
+    from oracle import projector as P
+    from tests.geoms import tiny
+    from tests.problems import synthetic_problem
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out, uid, tmax = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pb = synthetic_problem(tiny("helical_arc", na=43), M=4)
+    g, M = pb["geom"], 4
+    for m in range(M):
+        st, sd, cnt = subset_views(g["na"], M, m)
+        r = pb["w"][st::sd][:cnt] * (P.forward(g, pb["x0"], (st, sd, cnt)) - pb["y"][st::sd][:cnt])
+        full = M * P.back(g, r, (st, sd, cnt))
+        assert np.allclose(out[m], full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+    assert uid == bytes(range(128)) and tmax == 2.0
