@@ -124,6 +124,8 @@ static ct_status validate_desc(const ct_geom_desc* d) {
         const double c = std::cos(th);
         width = d->dsd * (diag / dmin) / (c * c) / d->ds;
     }
+    // corner-offset angle seen from the source (small-angle atan in ct_footprint)
+    if (0.5 * diag / dmin > 0.05) return fail(CT_E_CONFIG, "voxels too large for their distance to the source");
     if (width + 2.0 > kMaxCells)
         return fail(CT_E_CONFIG, "voxel footprint spans up to %.1f detector columns (limit %d)", width + 2.0,
                     kMaxCells);
@@ -309,8 +311,8 @@ static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dis
     off = align_up(off + sizeof(Ctl));
     L.xalt = off;
     off = align_up(off + sizeof(float) * g->G.nvox);
-    L.xt = off;
-    if (g->G.dim == 3) off = align_up(off + sizeof(float) * g->G.nvox);
+    L.xt = off;  // z-prefix array of x+ for the 3-D forward projector
+    if (g->G.dim == 3) off = align_up(off + sizeof(float) * (size_t)g->G.nxy * pfx_stride_of(g->G));
     L.r = off;
     off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
     L.zeta = off;
@@ -358,7 +360,7 @@ static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, flo
                             const float* kappa, float* r, int max_count, float M, float lo, float hi,
                             cudaStream_t s) {
     launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, xt, s);
-    if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, r, FWD_RESID, s, true);
+    if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, r, FWD_RESID, s, pfx_stride_of(g->G));
     else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
     launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);
     launch_advance(ctl, s);
@@ -492,7 +494,8 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
-            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s, true);
+            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s,
+                               pfx_stride_of(g->G));
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
             if (!dist) {

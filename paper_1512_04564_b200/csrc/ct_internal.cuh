@@ -89,61 +89,66 @@ struct Footprint {
     float B0, H;          // axial: voxel k spans row units [B0 + k H, B0 + (k+1) H]
 };
 
-// atan2 of a small angle given (sin-like, cos-like) components.
-__device__ __forceinline__ float small_atan2(float y, float x) { return atan2f(y, x); }
-
 // view: (cos beta, sin beta, z_s)
+// Arithmetic: the column centre's tau uses IEEE atan2f / division (it sets the
+// absolute position of the footprint on the detector); the corner offsets are
+// O(voxel) quantities, computed as atan(z) ~ z - z^3/3 + z^5/5 of z = cross/dot
+// (|z| < 0.05 in every supported geometry: truncation < 1e-8 relative) and
+// with fast reciprocals (__fdividef, rsqrtf: 2 ulp) -- DESIGN.md §5.
 template <bool ARC>
 __device__ __forceinline__ void ct_footprint(const DGeom& G, float cb, float sb, float zs, int i, int j,
                                              Footprint& f) {
     const float cx = fmaf((float)i, G.dx, G.x0);
     const float cy = fmaf((float)j, G.dy, G.y0);
-    const float rx = cx - G.dso * cb;
-    const float ry = cy - G.dso * sb;
+    const float rx = fmaf(-G.dso, cb, cx);
+    const float ry = fmaf(-G.dso, sb, cy);
     // frame of the view: a along e_c = -(cos,sin), b along e_u = (-sin, cos)
     const float a = -(rx * cb + ry * sb);
     const float b = ry * cb - rx * sb;
     const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
     // corner offsets (+-hx, +-hy) in (a, b): da = -(ex cb + ey sb), db = ey cb - ex sb
-    const float da1 = hx * cb, da2 = hy * sb;   // da = -(+-da1 +- da2)
-    const float db1 = hx * sb, db2 = hy * cb;   // db = (+-db2) - (+-db1)
+    const float da1 = hx * cb, da2 = hy * sb;
+    const float db1 = hx * sb, db2 = hy * cb;
+    const float r2 = fmaf(a, a, b * b);
+    const float inva = __fdividef(1.f, a);
     float t[4];
-    float tc;
 #pragma unroll
     for (int q = 0; q < 4; q++) {
         const float sx = (q & 1) ? 1.f : -1.f;
         const float sy = (q & 2) ? 1.f : -1.f;
         const float dA = -(sx * da1 + sy * da2);
         const float dB = sy * db2 - sx * db1;
+        const float cr = a * dB - b * dA;
         if (ARC) {
-            // angle(p_k) - angle(p_c) = atan2(a db - b da, a (a + da) + b (b + db))
-            const float cr = a * dB - b * dA;
-            const float dt_ = fmaf(a, a + dA, b * (b + dB));
-            t[q] = atan2f(cr, dt_);
+            // angle(p_k) - angle(p_c) = atan(cr / (a (a + da) + b (b + db)))
+            const float z = __fdividef(cr, r2 + fmaf(a, dA, b * dB));
+            const float z2 = z * z;
+            t[q] = z * fmaf(z2, fmaf(z2, 0.2f, -0.33333334f), 1.f);
         } else {
             // Dsd (b+db)/(a+da) - Dsd b/a = Dsd (db a - b da) / (a (a + da))
-            t[q] = G.dsd * (dB * a - b * dA) / (a * (a + dA));
+            t[q] = G.dsd * cr * inva * __fdividef(1.f, a + dA);
         }
     }
-    tc = ARC ? atan2f(b, a) : G.dsd * b / a;
+    const float tc = ARC ? atan2f(b, a) : G.dsd * b / a;
     sort4(t[0], t[1], t[2], t[3]);
     f.u0 = t[0] * G.inv_delta;
     f.u1 = t[1] * G.inv_delta;
     f.u2 = t[2] * G.inv_delta;
     f.u3 = t[3] * G.inv_delta;
     f.sfc = fmaf(tc, G.inv_delta, G.s_c0);
-    const float r1 = f.u1 - f.u0, r2 = f.u3 - f.u2;
-    f.inv2r1 = r1 > kRampEps ? 0.5f / r1 : 0.f;
-    f.halfr2 = r2 > kRampEps ? 0.5f * r2 : 0.f;
-    f.inv2r2 = r2 > kRampEps ? 0.5f / r2 : 0.f;
-    // L_xy = min(dx/|d_x|, dy/|d_y|) with d = (rx, ry)/|r|
-    const float rn = sqrtf(rx * rx + ry * ry);
+    const float w1 = f.u1 - f.u0, w2 = f.u3 - f.u2;
+    f.inv2r1 = w1 > kRampEps ? __fdividef(0.5f, w1) : 0.f;
+    f.halfr2 = w2 > kRampEps ? 0.5f * w2 : 0.f;
+    f.inv2r2 = w2 > kRampEps ? __fdividef(0.5f, w2) : 0.f;
+    // L_xy = min(dx/|d_x|, dy/|d_y|) with d = (rx, ry)/|r|, |r| = |(a, b)|
+    const float rinv = rsqrtf(r2);
+    const float rn = r2 * rinv;
     const float arx = fabsf(rx), ary = fabsf(ry);
-    const float lx = arx > 0.f ? G.dx * rn / arx : 3.0e38f;
-    const float ly = ary > 0.f ? G.dy * rn / ary : 3.0e38f;
+    const float lx = arx > 0.f ? __fdividef(G.dx * rn, arx) : 3.0e38f;
+    const float ly = ary > 0.f ? __fdividef(G.dy * rn, ary) : 3.0e38f;
     f.lxy = fminf(lx, ly);
     // axial magnification: flat Dsd/a, arc Dsd/|r|; row units u = t/dt + t_c0p
-    const float mag = ARC ? G.dsd / rn : G.dsd / a;
+    const float mag = ARC ? G.dsd * rinv : G.dsd * inva;
     const float mdt = mag * G.inv_dt;
     f.H = G.dz * mdt;
     f.B0 = fmaf(G.z0 - 0.5f * G.dz - zs, mdt, G.t_c0p);

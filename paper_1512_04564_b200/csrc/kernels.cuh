@@ -17,7 +17,10 @@ struct RegParams {
 // by this sub-iteration's update (parity of k - k_base), else xa.
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
                 const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
-                bool xt = false);
+                int pfx_stride = 0);  // > 0: xa is the z-prefix array (3-D solve path)
+
+// column stride (floats) of the z-prefix array: nz + 1 rounded up to 4
+__host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 1) + 3) & ~3; }
 
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);
@@ -28,7 +31,7 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
 
 // fused stencil + x-update of Algorithm 1 lines 4-5, writes htilde partial
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* xt,
+                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s);
 
 // dist path: g, htilde update from an all-reduced zeta (lines 7-8)

@@ -8,7 +8,8 @@
 // forward kernel), keeps F1 of its <= kMaxCells columns in a per-thread
 // shared-memory slot, forms the row sums rs(t) = L_xy sum_s F1(s) r[t][s] of
 // the rows its chunk projects to, then distributes them to its voxels with
-// the exact overlaps F2 (same boundary arithmetic as the forward's merge).
+// the exact overlaps F2, evaluated as differences of the cumulative row sum
+// at the voxel boundaries b_k = B0 + k H (one interpolation per voxel).
 //
 // Epilogues (Algorithm 1; htilde form):
 //   BK_WRITE   out = scale * A'r          BK_ACCUM out += scale * A'r
@@ -22,7 +23,7 @@ namespace ctr {
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
 constexpr int BK_KZ = 16;
-constexpr int BK_RMAX = 48;  // rows buffered per pass (more rows => several passes)
+constexpr int BK_RMAX = 36;  // rows buffered per pass (more rows => several passes)
 
 template <bool ARC, int DIM, int EPI, bool LZ>
 __global__ void __launch_bounds__(BK_BS)
@@ -31,6 +32,7 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
        float* __restrict__ htbuf) {
     __shared__ float f1s[kMaxCells][BK_BS];
     __shared__ float rsb[(DIM == 3) ? BK_RMAX : 1][BK_BS];
+    __shared__ float csb[(DIM == 3) ? BK_RMAX : 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
@@ -81,6 +83,10 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         }
         for (int tw = t0; tw <= t1; tw += BK_RMAX) {
             const int twe = min(t1, tw + BK_RMAX - 1);
+            // row sums rs(t) and their running sum C(t) = sum_{tw <= t' < t} rs(t'): the
+            // F2-weighted sum over the rows of voxel k is R(b_k+1) - R(b_k) with the
+            // piecewise-linear cumulative R(u) = C(floor u) + (u - floor u) rs(floor u).
+            float run = 0.f;
             for (int t = tw; t <= twe; t++) {
                 const float* __restrict__ pr = pv + (size_t)t * G.ns;
                 float rs = 0.f;
@@ -90,19 +96,23 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pr[q]), rs);
                 }
                 rsb[t - tw][tid] = rs;
+                csb[t - tw][tid] = run;
+                run += rs;
             }
+            const float ulo = (float)tw, uhi = (float)(twe + 1);
+            auto R = [&](float u) {
+                u = fminf(fmaxf(u, ulo), uhi);
+                const int t = min((int)u, twe);   // u >= tw >= 0: truncation = floor
+                const int o = t - tw;
+                return fmaf(u - (float)t, rsb[o][tid], csb[o][tid]);
+            };
+            float Rlo = R(voxel_b(f, k0));
 #pragma unroll
             for (int q = 0; q < BK_KZ; q++) {
                 if (q < kz) {
-                    const float lo = voxel_b(f, k0 + q), hi = voxel_b(f, k0 + q + 1);
-                    const int ta = max((int)floorf(lo), tw);
-                    const int tb = min((int)ceilf(hi) - 1, twe);
-                    float a = acc[q];
-                    for (int t = ta; t <= tb; t++) {
-                        const float ov = fminf(hi, (float)(t + 1)) - fmaxf(lo, (float)t);
-                        a = fmaf(ov, rsb[t - tw][tid], a);
-                    }
-                    acc[q] = a;
+                    const float Rhi = R(voxel_b(f, k0 + q + 1));
+                    acc[q] += Rhi - Rlo;
+                    Rlo = Rhi;
                 }
             }
         }

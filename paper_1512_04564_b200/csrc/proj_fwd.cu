@@ -176,26 +176,30 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
 
 
 // ---------------------------------------------------------------------------
-// 3-D forward projection, warp per detector column (v, s); lanes own detector
-// rows t = lane + 32 r.  The warp walks its column's fan wedge 8 slabs at a
-// time: lanes split the candidate voxel columns (4 per slab per pass),
-// evaluate their footprints in parallel, and push the columns with F1(s) > 0
-// into a warp queue (ballot + prefix popcount).  Every queued column is then
-// resampled onto the rows by all lanes at once: row t gathers the voxels
-// whose magnified z-extent [b_k, b_k+1] meets [t, t+1] (exact F2 overlaps,
-// same boundary arithmetic as the back-projector).  With XT the volume is
-// read in the z-fastest copy written by the x-update, so a lane group reads
-// one contiguous z-run per column (coalesced).  No atomics; row sums live in
-// registers; the epilogue stages the block's 8 columns through shared
-// memory so the residual kernel's y/w reads and r writes are 32-byte runs.
+// 3-D forward projection, warp per detector column (v, s); lane l owns the
+// RPL consecutive detector rows t = RPL*l + r.  The warp walks its column's
+// fan wedge 8 slabs at a time: lanes split the candidate voxel columns (4 per
+// slab per pass), evaluate their footprints in parallel and push the columns
+// with F1(s) > 0 into a warp queue (ballot + prefix popcount).  Each queued
+// column is then resampled onto the rows by all lanes at once.
+//   PFX (solve path): the x-update writes the z-prefix P_k = sum_{k'<k} x_k'
+//     of every voxel column (z-fastest, stride pfx_stride).  The magnified
+//     column is a piecewise-linear cumulative X(u) = H (P_k + frac x_k) over
+//     row units u, and the exact F2-weighted row sum is X(t+1) - X(t): RPL+1
+//     interpolations per lane, no per-voxel loop, no divergence.
+//   direct (ct_forward / init / D_L): row t loops over the voxels whose
+//     magnified extent [b_k, b_k+1] meets [t, t+1] (same overlap arithmetic as
+//     the back-projector), reading x in the boundary layout.
+// No atomics; row sums live in registers; the epilogue stages the block's 8
+// columns through shared memory so y/w reads and r writes are 32-byte runs.
 constexpr int F3_WARPS = 8;
 constexpr int F3_BS = 32 * F3_WARPS;
 
-template <bool ARC, int MODE, int RPL, bool XT>
+template <bool ARC, int MODE, int RPL, bool PFX>
 __global__ void __launch_bounds__(F3_BS)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
-       const float* __restrict__ w, float* __restrict__ out) {
+       const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
     __shared__ float4 qbuf[F3_WARPS][32];
     __shared__ float stage[32 * RPL][F3_WARPS + 1];
     constexpr bool ONES = (MODE == FWD_ONES_W);
@@ -207,7 +211,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const int s0 = blockIdx.x * F3_WARPS;
     const int s = s0 + wid;
     const float* __restrict__ x = xa;
-    if (ctl && !XT) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
+    if (ctl && !PFX) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
     const float4 vw = __ldg(&vtab[v]);
     const float cb = vw.x, sb = vw.y, zs = vw.z;
     const float Sx = G.dso * cb, Sy = G.dso * sb;
@@ -249,8 +253,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         const float kr = xstep ? dry / drx : drx / dry;
         const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
         const float inv_do = 1.f / dob;
-        const float nzH_dummy = 0.f;
-        (void)nzH_dummy;
+        const float fnz = (float)G.nz;
 
         for (int sl0 = 0; sl0 < na_; sl0 += 8) {
             const int sl = sl0 + (lane >> 2), sub = lane & 3;
@@ -284,7 +287,12 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         const float F1 = sf_F1(f, s);
                         if (F1 > 0.f) {
                             nz = true;
-                            ent = make_float4(f.lxy * F1, f.B0, f.H, __int_as_float(j * G.nx + i));
+                            if (PFX) {
+                                const float invH = 1.f / f.H;
+                                ent = make_float4(f.lxy * F1 * f.H, -f.B0 * invH, invH, __int_as_float(j * G.nx + i));
+                            } else {
+                                ent = make_float4(f.lxy * F1, f.B0, f.H, __int_as_float(j * G.nx + i));
+                            }
                         }
                     }
                 }
@@ -295,28 +303,43 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 for (int e = 0; e < n; e++) {
                     const float4 q = qbuf[wid][e];
                     const int col = __float_as_int(q.w);
-                    const float* __restrict__ xc = XT ? x + (size_t)col * G.nz : x + col;
-                    const size_t kst = XT ? 1 : (size_t)G.nxy;
-                    const float invH = 1.f / q.z;
-                    const float btop = fmaf((float)G.nz, q.z, q.y);
+                    if (PFX) {
+                        const float* __restrict__ pc = x + (size_t)col * pfx_stride;
+                        float Xp[RPL + 1];
 #pragma unroll
-                    for (int r = 0; r < RPL; r++) {
-                        const int t = lane + 32 * r;
-                        const float tb = (float)t, tb1 = (float)(t + 1);
-                        if (t < G.nt && tb1 > q.y && tb < btop) {
-                            int k = (int)floorf((tb - q.y) * invH);
-                            k = min(max(k, 0), G.nz - 1);
-                            while (k > 0 && fmaf((float)k, q.z, q.y) > tb) k--;
-                            float a = 0.f;
-                            float bk = fmaf((float)k, q.z, q.y);
-                            for (; k < G.nz; k++) {
-                                if (bk >= tb1) break;
-                                const float bk1 = fmaf((float)(k + 1), q.z, q.y);
-                                const float ov = fminf(bk1, tb1) - fmaxf(bk, tb);
-                                if (ov > 0.f) a = fmaf(ov, ONES ? 1.f : __ldg(&xc[(size_t)k * kst]), a);
-                                bk = bk1;
+                        for (int r = 0; r <= RPL; r++) {
+                            float f = fmaf((float)(RPL * lane + r), q.z, q.y);
+                            f = fminf(fmaxf(f, 0.f), fnz);
+                            const float fk = floorf(f);
+                            const int k = (int)fk;
+                            const float p0 = __ldg(&pc[k]);
+                            const float p1 = __ldg(&pc[min(k + 1, G.nz)]);
+                            Xp[r] = fmaf(f - fk, p1 - p0, p0);
+                        }
+#pragma unroll
+                        for (int r = 0; r < RPL; r++) acc[r] = fmaf(q.x, Xp[r + 1] - Xp[r], acc[r]);
+                    } else {
+                        const float* __restrict__ xc = x + col;
+                        const float btop = fmaf(fnz, q.z, q.y);
+#pragma unroll
+                        for (int r = 0; r < RPL; r++) {
+                            const int t = RPL * lane + r;
+                            const float tb = (float)t, tb1 = (float)(t + 1);
+                            if (t < G.nt && tb1 > q.y && tb < btop) {
+                                int k = (int)floorf((tb - q.y) / q.z);
+                                k = min(max(k, 0), G.nz - 1);
+                                while (k > 0 && fmaf((float)k, q.z, q.y) > tb) k--;
+                                float a = 0.f;
+                                float bk = fmaf((float)k, q.z, q.y);
+                                for (; k < G.nz; k++) {
+                                    if (bk >= tb1) break;
+                                    const float bk1 = fmaf((float)(k + 1), q.z, q.y);
+                                    const float ov = fminf(bk1, tb1) - fmaxf(bk, tb);
+                                    if (ov > 0.f) a = fmaf(ov, ONES ? 1.f : __ldg(&xc[(size_t)k * G.nxy]), a);
+                                    bk = bk1;
+                                }
+                                acc[r] = fmaf(q.x, a, acc[r]);
                             }
-                            acc[r] = fmaf(q.x, a, acc[r]);
                         }
                     }
                 }
@@ -327,7 +350,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 
     // epilogue: stage [row][column-in-block], then each thread handles one (row, col)
 #pragma unroll
-    for (int r = 0; r < RPL; r++) stage[lane + 32 * r][wid] = acc[r];
+    for (int r = 0; r < RPL; r++) stage[RPL * lane + r][wid] = acc[r];
     __syncthreads();
     for (int q = threadIdx.x; q < G.nt * F3_WARPS; q += F3_BS) {
         const int t = q / F3_WARPS, c = q % F3_WARPS;
@@ -347,27 +370,28 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 }
 
-template <bool ARC, int MODE, bool XT>
+template <bool ARC, int MODE, bool PFX>
 static void fwd3_rpl(const DGeom& G, dim3 grid, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
-                     const float* xb, const float* y, const float* w, float* out, cudaStream_t s) {
-    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-    else k_fwd3<ARC, MODE, 4, XT><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+                     const float* xb, const float* y, const float* w, float* out, int ps, cudaStream_t s) {
+    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    else k_fwd3<ARC, MODE, 4, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
 }
 
 template <bool ARC>
 static void fwd3_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                           const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
-                          bool xt, cudaStream_t s) {
+                          int pfx_stride, cudaStream_t s) {
     dim3 grid((G.ns + F3_WARPS - 1) / F3_WARPS, max_count);
+    const bool pfx = pfx_stride > 0;
     if (mode == FWD_PLAIN) {
-        xt ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s)
-           : fwd3_rpl<ARC, FWD_PLAIN, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+        pfx ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
+            : fwd3_rpl<ARC, FWD_PLAIN, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     } else if (mode == FWD_RESID) {
-        xt ? fwd3_rpl<ARC, FWD_RESID, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s)
-           : fwd3_rpl<ARC, FWD_RESID, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+        pfx ? fwd3_rpl<ARC, FWD_RESID, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
+            : fwd3_rpl<ARC, FWD_RESID, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     } else {
-        fwd3_rpl<ARC, FWD_ONES_W, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, s);
+        fwd3_rpl<ARC, FWD_ONES_W, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     }
 }
 
@@ -394,13 +418,14 @@ static void fwd_dispatch_mode(const DGeom& G, const float4* vtab, const Ctl* ctl
 }
 
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
-                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s, bool xt) {
+                const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
+                int pfx_stride) {
     if (max_count <= 0) return;
     if (G.arc) {
-        if (G.dim == 3) fwd3_dispatch<true>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, xt, s);
+        if (G.dim == 3) fwd3_dispatch<true>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, pfx_stride, s);
         else fwd_dispatch_mode<true, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     } else {
-        if (G.dim == 3) fwd3_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, xt, s);
+        if (G.dim == 3) fwd3_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, pfx_stride, s);
         else fwd_dispatch_mode<false, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     }
     launches_add(1);

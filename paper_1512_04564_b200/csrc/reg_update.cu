@@ -93,13 +93,6 @@ __global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float*
     if (curv) curv[idx] = cv;
 }
 
-// z-marching update: thread = voxel column (i, j) x UPD_KZ consecutive z; the
-// 3x3x3 neighbourhood of x (and kappa) lives in registers and advances one
-// plane per voxel (9 loads per voxel instead of 27).  Writes x+ in the
-// boundary layout (coalesced over i) and, for the forward projector, in the
-// z-fastest copy xt (two 16-byte stores per thread and column).
-constexpr int UPD_KZ = 8;
-
 template <int NDIRS, bool KAPPA, int POT>
 __device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const float (&K)[3][3][3],
                                                const RegParams& rp, bool im, bool ip, bool jm, bool jp, bool km,
@@ -129,26 +122,37 @@ __device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const 
     curv = 2.f * cs;
 }
 
+// Fused stencil + x-update, z-marching: thread = one voxel column (i, j), all
+// nz voxels; a warp = 32 consecutive i at one j.  The 3x3x3 neighbourhood of x
+// (and kappa) lives in registers and advances one plane per voxel (9 loads per
+// voxel instead of 27).  x+ and htilde_partial are written in the boundary
+// layout (coalesced over i).  With pfx != nullptr the thread also forms the
+// z-prefix P_k = sum_{k'<k} x+_k' of its column for the forward projector;
+// 32 prefix values per column are staged in shared memory and written as
+// whole 128-byte lines (z-fastest layout, column stride pfx_stride_of(G)).
 template <int POT, int NDIRS, bool KAPPA>
 __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
                                                 float* xb, const float* __restrict__ dl,
                                                 const float* __restrict__ g, float* __restrict__ ht,
                                                 const float* __restrict__ kappa, float box_lo, float box_hi,
-                                                float* __restrict__ xt) {
-    const int i = blockIdx.x * 32 + threadIdx.x;
-    const int j = blockIdx.y * 4 + threadIdx.y;
-    const int k0 = blockIdx.z * UPD_KZ;
-    if (i >= G.nx || j >= G.ny) return;
+                                                float* __restrict__ pfx) {
+    __shared__ float pst[4][32][33];
+    const int lane = threadIdx.x, wy = threadIdx.y;
+    const int i = blockIdx.x * 32 + lane;
+    const int j = blockIdx.y * 4 + wy;
+    const bool act = i < G.nx && j < G.ny;
+    if (j >= G.ny) return;  // warp-uniform (whole warp shares j)
     const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
     const float* __restrict__ x = odd ? xb : xa;
     float* __restrict__ xn = odd ? xa : xb;
     const float rho = rho_of_k(ctl);
     const float alpha = ctl->alpha;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
-    const size_t col = (size_t)j * G.nx + i;
+    const size_t col = (size_t)j * G.nx + (act ? i : 0);
+    const int ps = pfx_stride_of(G);
     float W[3][3][3], K[3][3][3];
     auto load_plane = [&](int slot, int k) {
-        const bool ok = k >= 0 && k < G.nz;
+        const bool ok = act && k >= 0 && k < G.nz;
 #pragma unroll
         for (int dy = -1; dy <= 1; dy++) {
 #pragma unroll
@@ -160,28 +164,34 @@ __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl
             }
         }
     };
-    load_plane(0, k0 - 1);
-    load_plane(1, k0);
-    float xo[UPD_KZ];
+    auto flush = [&](int kb, int n) {  // prefix entries kb .. kb+n-1 of the warp's 32 columns
+        __syncwarp();
+        const int cbase = blockIdx.x * 32;
+        for (int c = 0; c < 32; c++) {
+            if (cbase + c < G.nx && lane < n)
+                pfx[((size_t)j * G.nx + cbase + c) * ps + kb + lane] = pst[wy][lane][c];
+        }
+        __syncwarp();
+    };
+    load_plane(1, -1);
+    load_plane(2, 0);
+    float run = 0.f;
+    int kb = 0;
+    for (int k = 0; k < G.nz; k++) {
 #pragma unroll
-    for (int kk = 0; kk < UPD_KZ; kk++) {
-        const int k = k0 + kk;
-        xo[kk] = 0.f;
-        if (k < G.nz) {
-            if (kk > 0) {
+        for (int a = 0; a < 3; a++)
 #pragma unroll
-                for (int a = 0; a < 3; a++)
-#pragma unroll
-                    for (int b = 0; b < 3; b++) {
-                        W[0][a][b] = W[1][a][b];
-                        W[1][a][b] = W[2][a][b];
-                        if (KAPPA) {
-                            K[0][a][b] = K[1][a][b];
-                            K[1][a][b] = K[2][a][b];
-                        }
-                    }
+            for (int b = 0; b < 3; b++) {
+                W[0][a][b] = W[1][a][b];
+                W[1][a][b] = W[2][a][b];
+                if (KAPPA) {
+                    K[0][a][b] = K[1][a][b];
+                    K[1][a][b] = K[2][a][b];
+                }
             }
-            load_plane(2, k + 1);
+        load_plane(2, k + 1);
+        float xnew = 0.f;
+        if (act) {
             float gr, cv;
             window_stencil<NDIRS, KAPPA, POT>(W, K, rp, im, ip, jm, jp, k > 0, k + 1 < G.nz, gr, cv);
             const size_t idx = (size_t)k * G.nxy + col;
@@ -190,23 +200,23 @@ __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl
             const float htv = ht[idx];
             const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
             const float den = fmaf(rho, d, cv);
-            float xnew = xv;
+            xnew = xv;
             if (den > 0.f) xnew = fminf(fmaxf(xv - (s + gr) / den, box_lo), box_hi);
             xn[idx] = xnew;
             ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
-            xo[kk] = xnew;
+        }
+        if (pfx) {
+            pst[wy][k - kb][lane] = run;   // P_k (prefix before voxel k)
+            run += xnew;
+            if (k - kb == 31) {
+                flush(kb, 32);
+                kb += 32;
+            }
         }
     }
-    if (xt) {
-        float* dst = xt + col * G.nz + k0;
-        if (k0 + UPD_KZ <= G.nz && (G.nz & 3) == 0) {
-            reinterpret_cast<float4*>(dst)[0] = make_float4(xo[0], xo[1], xo[2], xo[3]);
-            reinterpret_cast<float4*>(dst)[1] = make_float4(xo[4], xo[5], xo[6], xo[7]);
-        } else {
-#pragma unroll
-            for (int kk = 0; kk < UPD_KZ; kk++)
-                if (k0 + kk < G.nz) dst[kk] = xo[kk];
-        }
+    if (pfx) {
+        pst[wy][G.nz - kb][lane] = run;  // P_nz
+        flush(kb, G.nz - kb + 1);
     }
 }
 
@@ -231,21 +241,21 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
 
 template <int POT, int NDIRS>
 static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                         const float* g, float* ht, const float* kappa, float lo, float hi, float* xt,
+                         const float* g, float* ht, const float* kappa, float lo, float hi, float* pfx,
                          cudaStream_t s) {
-    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4, (G.nz + UPD_KZ - 1) / UPD_KZ);
-    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, xt);
-    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, xt);
+    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4, 1);
+    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx);
+    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx);
 }
 
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* xt,
+                   const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s) {
     const bool d4 = rp.n_dirs == 4;
     switch (rp.potential) {
-        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
-        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
-        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, xt, s); break;
+        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
+        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
+        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
     }
     launches_add(1);
 }
