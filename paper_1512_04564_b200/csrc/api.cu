@@ -213,6 +213,8 @@ static ct_status check_views(const ct_geom* g, ct_views v) {
     if (v.start < 0 || last >= g->d.na)
         return fail(CT_E_SHAPE, "views {%d,%d,%d} outside [0, %d)", v.start, v.stride, v.count, g->d.na);
     if (v.count > 65535) return fail(CT_E_SHAPE, "at most 65535 views per call (got %d)", v.count);
+    if ((long long)v.count * g->G.nt * g->G.ns >= (1LL << 31))
+        return fail(CT_E_SHAPE, "projection block of %d views exceeds 2^31 elements", v.count);
     return CT_OK;
 }
 
@@ -398,6 +400,8 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     const int M = p->M;
     const int vm_max = (g->d.na + M - 1) / M;
     const int max_count = (vm_max + world - 1) / world;
+    if ((long long)max_count * g->G.nt * g->G.ns >= (1LL << 31))
+        return fail(CT_E_SHAPE, "subset projection block exceeds 2^31 elements (increase M)");
     const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
 
     Ctl h;

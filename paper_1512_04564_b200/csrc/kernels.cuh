@@ -19,8 +19,8 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
                 const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
                 int pfx_stride = 0);  // > 0: xa is the z-prefix array (3-D solve path)
 
-// column stride (floats) of the z-prefix array: nz + 1 rounded up to 4
-__host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 1) + 3) & ~3; }
+// column stride (floats) of the z-prefix array P_0..P_nz, P_nz+1 (= P_nz): nz + 2 rounded up to 4
+__host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 2) + 3) & ~3; }
 
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);

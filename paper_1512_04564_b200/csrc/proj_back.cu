@@ -22,7 +22,7 @@ namespace ctr {
 
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ = 16;
+constexpr int BK_KZ = 32;
 constexpr int BK_RMAX = 36;  // rows buffered per pass (more rows => several passes)
 
 template <bool ARC, int DIM, int EPI, bool LZ>
@@ -74,10 +74,10 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 Tprev = Tn;
             }
         }
-        const float* __restrict__ pv = proj + (size_t)vi * nt * G.ns + slo;
+        const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns + (unsigned)slo;  // < 2^32 (checked at launch)
         if (DIM != 3) {
             float rs = 0.f;
-            for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pv[q]), rs);
+            for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(proj + (pv + q)), rs);
             acc[0] += rs;
             continue;
         }
@@ -88,7 +88,7 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
             // piecewise-linear cumulative R(u) = C(floor u) + (u - floor u) rs(floor u).
             float run = 0.f;
             for (int t = tw; t <= twe; t++) {
-                const float* __restrict__ pr = pv + (size_t)t * G.ns;
+                const float* __restrict__ pr = proj + (pv + (unsigned)t * (unsigned)G.ns);
                 float rs = 0.f;
                 if (LZ) {
                     for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid] * ray_Lz<ARC>(G, slo + q, t), __ldg(&pr[q]), rs);

@@ -288,7 +288,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         if (F1 > 0.f) {
                             nz = true;
                             if (PFX) {
-                                const float invH = 1.f / f.H;
+                                const float invH = __fdividef(1.f, f.H);
                                 ent = make_float4(f.lxy * F1 * f.H, -f.B0 * invH, invH, __int_as_float(j * G.nx + i));
                             } else {
                                 ent = make_float4(f.lxy * F1, f.B0, f.H, __int_as_float(j * G.nx + i));
@@ -304,16 +304,21 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const float4 q = qbuf[wid][e];
                     const int col = __float_as_int(q.w);
                     if (PFX) {
-                        const float* __restrict__ pc = x + (size_t)col * pfx_stride;
+                        // column base (32-bit element index); P has entries 0..nz+1 (P_nz+1 = P_nz)
+                        const unsigned cbase = (unsigned)col * (unsigned)pfx_stride;
                         float Xp[RPL + 1];
 #pragma unroll
                         for (int r = 0; r <= RPL; r++) {
                             float f = fmaf((float)(RPL * lane + r), q.z, q.y);
                             f = fminf(fmaxf(f, 0.f), fnz);
-                            const float fk = floorf(f);
-                            const int k = (int)fk;
-                            const float p0 = __ldg(&pc[k]);
-                            const float p1 = __ldg(&pc[min(k + 1, G.nz)]);
+                            // k = round-to-nearest(f - 1/2) via the 1.5*2^23 magic number, so
+                            // k <= f <= k+1 (at an integer f either neighbouring segment gives the
+                            // same X: X is continuous).  f - 1/2 is exact for 0 <= f < 2^22.
+                            const float rm = __fadd_rn(__fadd_rn(f, -0.5f), 12582912.0f);
+                            const int k = __float_as_int(rm) - 0x4B400000;
+                            const float fk = rm - 12582912.0f;
+                            const float* __restrict__ pp = x + (cbase + (unsigned)k);
+                            const float p0 = __ldg(pp), p1 = __ldg(pp + 1);
                             Xp[r] = fmaf(f - fk, p1 - p0, p0);
                         }
 #pragma unroll

@@ -176,7 +176,15 @@ __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl
     load_plane(1, -1);
     load_plane(2, 0);
     float run = 0.f;
-    int kb = 0;
+    int kb = 0, cnt = 0;
+    auto push = [&](float v) {
+        pst[wy][cnt][lane] = v;
+        if (++cnt == 32) {
+            flush(kb, 32);
+            kb += 32;
+            cnt = 0;
+        }
+    };
     for (int k = 0; k < G.nz; k++) {
 #pragma unroll
         for (int a = 0; a < 3; a++)
@@ -206,17 +214,14 @@ __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl
             ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
         }
         if (pfx) {
-            pst[wy][k - kb][lane] = run;   // P_k (prefix before voxel k)
+            push(run);   // P_k: prefix before voxel k
             run += xnew;
-            if (k - kb == 31) {
-                flush(kb, 32);
-                kb += 32;
-            }
         }
     }
     if (pfx) {
-        pst[wy][G.nz - kb][lane] = run;  // P_nz
-        flush(kb, G.nz - kb + 1);
+        push(run);  // P_nz
+        push(run);  // P_nz+1 = P_nz (padding read by the forward's interpolation)
+        if (cnt) flush(kb, cnt);
     }
 }
 

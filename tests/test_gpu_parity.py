@@ -254,3 +254,61 @@ def test_deterministic_repeat(C):
         outs.append(host(rec.x))
         rec.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name", ["c4", "c3", "c2"])
+def test_full_size_subiteration_sampled(C, name):
+    """BASELINE config at full size, bench launch configuration (graph-replayed
+    solve): one sub-iteration from a seeded state (k = 5, so subset 5 and
+    rho_5), compared with the oracle: x+ on every voxel; g+ and htilde+ on
+    sampled voxels (the oracle back-projects the subset residual of its own
+    x+ at those voxels)."""
+    from oracle import alg
+    from paper_1512_04564_b200.recon import Recon
+    from synth.configs import get_config, reg_betas
+    from synth.data import make_dataset
+    cfg = get_config(name)
+    g = cfg["geom"]
+    M, alpha = cfg["solver"]["M"], cfg["solver"]["alpha"]
+    data = make_dataset(cfg, device="cuda")
+    y = data["y"].double().cpu().numpy()
+    w = data["w"].double().cpu().numpy()
+    x = data["x0"].double().cpu().numpy()
+    shape = x.shape
+    rng = np.random.default_rng(11)
+    # seeded state: smooth positive D_L of the right scale, gradient-scale g and htilde
+    dl = (0.5 + rng.random(shape)) * cfg["reg"]["beta0"] * 40.0
+    gg = rng.standard_normal(shape) * cfg["reg"]["beta0"] * 1e-3
+    ht = rng.standard_normal(shape) * cfg["reg"]["beta0"] * 1e-3
+    nd = cfg["reg"]["n_dirs"]
+    reg = dict(potential="hyperbola", delta=cfg["reg"]["delta"], betas=reg_betas(g, cfg["reg"]["beta0"], nd),
+               n_dirs=nd)
+    k0 = 5
+    rec = Recon(g, reg, cfg["solver"], data["y"], data["w"], x)
+    rec.set_DL(dl)
+    rec.g.copy_(torch.as_tensor(gg, dtype=torch.float32))
+    rec.htilde.copy_(torch.as_tensor(ht, dtype=torch.float32))
+    rec.state.k = k0
+    # the device state is float32: feed the oracle the same rounded inputs
+    x32, g32, h32, dl32 = (np.asarray(np.float32(a), dtype=np.float64) for a in (x, gg, ht, dl))
+    rec.run(1)
+    xg, gg_gpu, ht_gpu = host(rec.x), host(rec.g), host(rec.htilde)
+    rec.close()
+    # oracle, Alg. 1 lines 4-8 in the paper's variables (h = D_L x - htilde)
+    prob = alg.Problem(g, y, w, reg["potential"], reg["delta"], reg["betas"], nd)
+    h = dl32 * x32 - h32
+    rho = alg.rho_k(k0, alpha)
+    gradR, DR = prob.reg(x32)
+    s = rho * (dl32 * x32 - h) + (1 - rho) * g32
+    xo = np.maximum(x32 - (s + gradR) / (rho * dl32 + DR), 0.0)
+    assert rel(xg, xo) <= 1e-5, rel(xg, xo)
+    m = k0 % M
+    views = (m, M, (g["na"] - m + M - 1) // M)
+    r = w[m::M][:views[2]] * (P.forward(g, xo, views) - y[m::M][:views[2]])
+    idx = np.sort(rng.choice(xo.size, 400, replace=False))
+    zeta = M * P.back_voxels(g, r, views, idx)
+    go = rho / (rho + 1) * (alpha * zeta + (1 - alpha) * g32.ravel()[idx]) + g32.ravel()[idx] / (rho + 1)
+    ho = alpha * (dl32.ravel()[idx] * xo.ravel()[idx] - zeta) + (1 - alpha) * h.ravel()[idx]
+    assert rel(gg_gpu.ravel()[idx], go) <= 1e-4, rel(gg_gpu.ravel()[idx], go)
+    hto = dl32.ravel()[idx] * xo.ravel()[idx] - ho
+    assert rel(ht_gpu.ravel()[idx], hto) <= 1e-4, rel(ht_gpu.ravel()[idx], hto)
