@@ -176,12 +176,17 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
 
 
 // ---------------------------------------------------------------------------
-// 3-D forward projection, warp per detector column (v, s); lane l owns the
-// RPL consecutive detector rows t = RPL*l + r.  The warp walks its column's
-// fan wedge 8 slabs at a time: lanes split the candidate voxel columns (4 per
-// slab per pass), evaluate their footprints in parallel and push the columns
-// with F1(s) > 0 into a warp queue (ballot + prefix popcount).  Each queued
-// column is then resampled onto the rows by all lanes at once.
+// 3-D forward projection.  A warp owns F3_CPW = 4 adjacent detector columns
+// s0..s0+3 of one view (the union of their fan wedges); lane l owns the RPL
+// consecutive detector rows t = RPL*l + r of all four columns.  The warp walks
+// the union wedge 8 slabs at a time: lanes split the candidate voxel columns
+// (4 per slab per pass), evaluate their footprints in parallel (ct_footprint,
+// shared with the back-projector; F1 for the four detector columns) and push
+// the voxel columns with any F1 > 0 into a warp queue (ballot + prefix
+// popcount).  Each queued voxel column is resampled onto the rows once and
+// credited to the four detector columns with their own L = L_xy F1 (a voxel
+// column's footprint covers ~2.4 detector columns, so this removes most of the
+// redundant resampling of a one-column-per-warp walk).
 //   PFX (solve path): the x-update writes the z-prefix P_k = sum_{k'<k} x_k'
 //     of every voxel column (z-fastest, stride pfx_stride).  The magnified
 //     column is a piecewise-linear cumulative X(u) = H (P_k + frac x_k) over
@@ -190,26 +195,30 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
 //   direct (ct_forward / init / D_L): row t loops over the voxels whose
 //     magnified extent [b_k, b_k+1] meets [t, t+1] (same overlap arithmetic as
 //     the back-projector), reading x in the boundary layout.
-// No atomics; row sums live in registers; the epilogue stages the block's 8
-// columns through shared memory so y/w reads and r writes are 32-byte runs.
+// No atomics; row sums live in registers; the epilogue stages the block's 32
+// detector columns through shared memory so y/w reads and r writes are
+// 128-byte runs.
 constexpr int F3_WARPS = 8;
+constexpr int F3_CPW = 4;
 constexpr int F3_BS = 32 * F3_WARPS;
+constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
 template <bool ARC, int MODE, int RPL, bool PFX>
 __global__ void __launch_bounds__(F3_BS)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
-    __shared__ float4 qbuf[F3_WARPS][32];
-    __shared__ float stage[32 * RPL][F3_WARPS + 1];
+    __shared__ float4 qL[F3_WARPS][32];    // L for the 4 detector columns
+    __shared__ float4 qG[F3_WARPS][32];    // PFX: (-B0/H, 1/H, col, -) ; direct: (B0, H, col, -)
+    __shared__ float stage[32 * RPL][F3_CPB + 1];
     constexpr bool ONES = (MODE == FWD_ONES_W);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const Views V = select_views(ctl, vsel);
     const int vi = blockIdx.y;
     if (vi >= V.count) return;
     const int v = V.start + vi * V.stride;
-    const int s0 = blockIdx.x * F3_WARPS;
-    const int s = s0 + wid;
+    const int sb0 = blockIdx.x * F3_CPB;          // first detector column of the block
+    const int s0 = sb0 + wid * F3_CPW;             // first detector column of the warp
     const float* __restrict__ x = xa;
     if (ctl && !PFX) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
     const float4 vw = __ldg(&vtab[v]);
@@ -217,14 +226,17 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const float Sx = G.dso * cb, Sy = G.dso * sb;
     const unsigned lanemask_lt = (1u << lane) - 1u;
 
-    float acc[RPL];
+    float acc[F3_CPW][RPL];
 #pragma unroll
-    for (int r = 0; r < RPL; r++) acc[r] = 0.f;
+    for (int c = 0; c < F3_CPW; c++)
+#pragma unroll
+        for (int r = 0; r < RPL; r++) acc[c][r] = 0.f;
 
-    if (s < G.ns) {  // warp-uniform
-        const float tl = ((float)s - 0.5f - G.s_c0) * G.delta;
-        const float tr = ((float)s + 0.5f - G.s_c0) * G.delta;
-        const float tm = ((float)s - G.s_c0) * G.delta;
+    if (s0 < G.ns) {  // warp-uniform
+        const int s3 = min(s0 + F3_CPW - 1, G.ns - 1);
+        const float tl = ((float)s0 - 0.5f - G.s_c0) * G.delta;
+        const float tr = ((float)s3 + 0.5f - G.s_c0) * G.delta;
+        const float tm = (0.5f * (float)(s0 + s3) - G.s_c0) * G.delta;
         float cal, cul, car, cur_, cam, cum;
         if (ARC) {
             sincosf(tl, &cul, &cal);
@@ -267,8 +279,8 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - o0) * inv_do + 0.5f;
                     const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - o0) * inv_do + 0.5f;
                     if (f1 >= -1.f && f0 <= (float)no_ + 1.f) {
-                        lo = max((int)floorf(f0) - 1, 0);
-                        hi = min((int)floorf(f1) + 1, no_ - 1);
+                        lo = max((int)floorf(f0 - 1e-3f), 0);
+                        hi = min((int)floorf(f1 + 1e-3f), no_ - 1);
                     }
                 }
             }
@@ -276,7 +288,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
             for (int p = 0; p < npass; p++) {
                 const int o = lo + sub + 4 * p;
                 bool nz = false;
-                float4 ent = make_float4(0.f, 0.f, 0.f, 0.f);
+                float4 eL = make_float4(0.f, 0.f, 0.f, 0.f), eG = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (o <= hi) {
                     const int i = xstep ? sl : o, j = xstep ? o : sl;
                     const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
@@ -284,32 +296,48 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     if (fmaf(nlx, cx, nly * cy) + suppl >= -tol_l && fmaf(nrx, cx, nry * cy) + suppr >= -tol_r) {
                         Footprint f;
                         ct_footprint<ARC>(G, cb, sb, zs, i, j, f);
-                        const float F1 = sf_F1(f, s);
-                        if (F1 > 0.f) {
+                        // F1 of the 4 detector columns from 5 edge evaluations
+                        float T0 = trap_T(f, ((float)s0 - 0.5f) - f.sfc);
+                        float Fc[F3_CPW];
+#pragma unroll
+                        for (int c = 0; c < F3_CPW; c++) {
+                            const float T1 = trap_T(f, ((float)(s0 + c) + 0.5f) - f.sfc);
+                            Fc[c] = (s0 + c < G.ns) ? T1 - T0 : 0.f;
+                            T0 = T1;
+                        }
+                        if (Fc[0] > 0.f || Fc[1] > 0.f || Fc[2] > 0.f || Fc[3] > 0.f) {
                             nz = true;
+                            const float Ls = PFX ? f.lxy * f.H : f.lxy;
+                            eL = make_float4(Ls * Fc[0], Ls * Fc[1], Ls * Fc[2], Ls * Fc[3]);
                             if (PFX) {
                                 const float invH = __fdividef(1.f, f.H);
-                                ent = make_float4(f.lxy * F1 * f.H, -f.B0 * invH, invH, __int_as_float(j * G.nx + i));
+                                eG = make_float4(-f.B0 * invH, invH, __int_as_float(j * G.nx + i), 0.f);
                             } else {
-                                ent = make_float4(f.lxy * F1, f.B0, f.H, __int_as_float(j * G.nx + i));
+                                eG = make_float4(f.B0, f.H, __int_as_float(j * G.nx + i), 0.f);
                             }
                         }
                     }
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, nz);
-                if (nz) qbuf[wid][__popc(m & lanemask_lt)] = ent;
+                if (nz) {
+                    const int slot = __popc(m & lanemask_lt);
+                    qL[wid][slot] = eL;
+                    qG[wid][slot] = eG;
+                }
                 __syncwarp();
                 const int n = __popc(m);
                 for (int e = 0; e < n; e++) {
-                    const float4 q = qbuf[wid][e];
-                    const int col = __float_as_int(q.w);
+                    const float4 L4 = qL[wid][e];
+                    const float4 q = qG[wid][e];
+                    const int col = __float_as_int(q.z);
+                    float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
                         // column base (32-bit element index); P has entries 0..nz+1 (P_nz+1 = P_nz)
                         const unsigned cbase = (unsigned)col * (unsigned)pfx_stride;
                         float Xp[RPL + 1];
 #pragma unroll
                         for (int r = 0; r <= RPL; r++) {
-                            float f = fmaf((float)(RPL * lane + r), q.z, q.y);
+                            float f = fmaf((float)(RPL * lane + r), q.y, q.x);
                             f = fminf(fmaxf(f, 0.f), fnz);
                             // k = round-to-nearest(f - 1/2) via the 1.5*2^23 magic number, so
                             // k <= f <= k+1 (at an integer f either neighbouring segment gives the
@@ -322,30 +350,37 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             Xp[r] = fmaf(f - fk, p1 - p0, p0);
                         }
 #pragma unroll
-                        for (int r = 0; r < RPL; r++) acc[r] = fmaf(q.x, Xp[r + 1] - Xp[r], acc[r]);
+                        for (int r = 0; r < RPL; r++) Rs[r] = Xp[r + 1] - Xp[r];
                     } else {
                         const float* __restrict__ xc = x + col;
-                        const float btop = fmaf(fnz, q.z, q.y);
+                        const float btop = fmaf(fnz, q.y, q.x);
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
                             const int t = RPL * lane + r;
                             const float tb = (float)t, tb1 = (float)(t + 1);
-                            if (t < G.nt && tb1 > q.y && tb < btop) {
-                                int k = (int)floorf((tb - q.y) / q.z);
+                            float a = 0.f;
+                            if (t < G.nt && tb1 > q.x && tb < btop) {
+                                int k = (int)floorf((tb - q.x) / q.y);
                                 k = min(max(k, 0), G.nz - 1);
-                                while (k > 0 && fmaf((float)k, q.z, q.y) > tb) k--;
-                                float a = 0.f;
-                                float bk = fmaf((float)k, q.z, q.y);
+                                while (k > 0 && fmaf((float)k, q.y, q.x) > tb) k--;
+                                float bk = fmaf((float)k, q.y, q.x);
                                 for (; k < G.nz; k++) {
                                     if (bk >= tb1) break;
-                                    const float bk1 = fmaf((float)(k + 1), q.z, q.y);
+                                    const float bk1 = fmaf((float)(k + 1), q.y, q.x);
                                     const float ov = fminf(bk1, tb1) - fmaxf(bk, tb);
                                     if (ov > 0.f) a = fmaf(ov, ONES ? 1.f : __ldg(&xc[(size_t)k * G.nxy]), a);
                                     bk = bk1;
                                 }
-                                acc[r] = fmaf(q.x, a, acc[r]);
                             }
+                            Rs[r] = a;
                         }
+                    }
+#pragma unroll
+                    for (int r = 0; r < RPL; r++) {
+                        acc[0][r] = fmaf(L4.x, Rs[r], acc[0][r]);
+                        acc[1][r] = fmaf(L4.y, Rs[r], acc[1][r]);
+                        acc[2][r] = fmaf(L4.z, Rs[r], acc[2][r]);
+                        acc[3][r] = fmaf(L4.w, Rs[r], acc[3][r]);
                     }
                 }
                 __syncwarp();
@@ -353,13 +388,15 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         }
     }
 
-    // epilogue: stage [row][column-in-block], then each thread handles one (row, col)
+    // epilogue: stage [row][detector column in block], then each thread handles one (row, column)
 #pragma unroll
-    for (int r = 0; r < RPL; r++) stage[RPL * lane + r][wid] = acc[r];
+    for (int c = 0; c < F3_CPW; c++)
+#pragma unroll
+        for (int r = 0; r < RPL; r++) stage[RPL * lane + r][wid * F3_CPW + c] = acc[c][r];
     __syncthreads();
-    for (int q = threadIdx.x; q < G.nt * F3_WARPS; q += F3_BS) {
-        const int t = q / F3_WARPS, c = q % F3_WARPS;
-        const int ss = s0 + c;
+    for (int q = threadIdx.x; q < G.nt * F3_CPB; q += F3_BS) {
+        const int t = q / F3_CPB, c = q % F3_CPB;
+        const int ss = sb0 + c;
         if (ss >= G.ns) continue;
         const float lz = ray_Lz<ARC>(G, ss, t);
         const float p = lz * stage[t][c];
@@ -387,7 +424,7 @@ template <bool ARC>
 static void fwd3_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                           const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
                           int pfx_stride, cudaStream_t s) {
-    dim3 grid((G.ns + F3_WARPS - 1) / F3_WARPS, max_count);
+    dim3 grid((G.ns + F3_CPB - 1) / F3_CPB, max_count);
     const bool pfx = pfx_stride > 0;
     if (mode == FWD_PLAIN) {
         pfx ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
