@@ -263,8 +263,7 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
     }
     ct_status st = check_async();
     if (st != CT_OK) return st;
-    if (dist && dist->world > 1)
-        CT_NCCL(ncclAllReduce(d_out, d_out, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, cs));
+    if (dist) CT_NCCL(ncclAllReduce(d_out, d_out, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, cs));
     return CT_OK;
 }
 
@@ -444,8 +443,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             }
             if (first) CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
         }
-        if (dist && dist->world > 1)
-            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+        if (dist) CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
         launch_init_from_zeta(g->G, zdst, st->g, st->htilde, s);
         stt = check_async();
         if (stt != CT_OK) return stt;
@@ -509,8 +507,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             } else {
                 launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
                 if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
-                if (dist->world > 1)
-                    CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+                CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
                 launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
             }
             launch_advance(ctl, s);

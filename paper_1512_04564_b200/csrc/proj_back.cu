@@ -22,8 +22,8 @@ namespace ctr {
 
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ = 32;
-constexpr int BK_RMAX = 36;  // rows buffered per pass (more rows => several passes)
+constexpr int BK_KZ = 16;
+constexpr int BK_RMAX = 48;  // rows buffered per pass (more rows => several passes)
 
 template <bool ARC, int DIM, int EPI, bool LZ>
 __global__ void __launch_bounds__(BK_BS)
@@ -31,8 +31,7 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
        const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
        float* __restrict__ htbuf) {
     __shared__ float f1s[kMaxCells][BK_BS];
-    __shared__ float rsb[(DIM == 3) ? BK_RMAX : 1][BK_BS];
-    __shared__ float csb[(DIM == 3) ? BK_RMAX : 1][BK_BS];
+    __shared__ float csb[(DIM == 3) ? BK_RMAX + 2 : 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
@@ -83,10 +82,12 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         }
         for (int tw = t0; tw <= t1; tw += BK_RMAX) {
             const int twe = min(t1, tw + BK_RMAX - 1);
-            // row sums rs(t) and their running sum C(t) = sum_{tw <= t' < t} rs(t'): the
-            // F2-weighted sum over the rows of voxel k is R(b_k+1) - R(b_k) with the
-            // piecewise-linear cumulative R(u) = C(floor u) + (u - floor u) rs(floor u).
+            // row sums rs(t) -> running sums cs[o] = sum_{tw <= t < tw+o} rs(t) (cs[n+1] = cs[n]
+            // pads the top).  The F2-weighted sum over the rows of voxel k is R(b_k+1) - R(b_k)
+            // with the piecewise-linear cumulative R(u) = cs[o] + frac (cs[o+1] - cs[o]).
+            const int n = twe - tw + 1;
             float run = 0.f;
+            csb[0][tid] = 0.f;
             for (int t = tw; t <= twe; t++) {
                 const float* __restrict__ pr = proj + (pv + (unsigned)t * (unsigned)G.ns);
                 float rs = 0.f;
@@ -95,16 +96,19 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 } else {
                     for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pr[q]), rs);
                 }
-                rsb[t - tw][tid] = rs;
-                csb[t - tw][tid] = run;
                 run += rs;
+                csb[t - tw + 1][tid] = run;
             }
-            const float ulo = (float)tw, uhi = (float)(twe + 1);
+            csb[n + 1][tid] = run;
+            const float shift = (float)tw + 0.5f, vmax = (float)n - 0.5f;
             auto R = [&](float u) {
-                u = fminf(fmaxf(u, ulo), uhi);
-                const int t = min((int)u, twe);   // u >= tw >= 0: truncation = floor
-                const int o = t - tw;
-                return fmaf(u - (float)t, rsb[o][tid], csb[o][tid]);
+                // o = round(v - 1/2), v = u - tw in [0, n]: o <= v <= o + 1 (magic-number floor)
+                const float vv = fminf(fmaxf(u - shift, -0.5f), vmax);
+                const float rm = __fadd_rn(vv, 12582912.0f);
+                const int o = __float_as_int(rm) - 0x4B400000;
+                const float fr = (vv + 0.5f) - (rm - 12582912.0f);
+                const float c0 = csb[o][tid];
+                return fmaf(fr, csb[o + 1][tid] - c0, c0);
             };
             float Rlo = R(voxel_b(f, k0));
 #pragma unroll

@@ -312,3 +312,24 @@ def test_full_size_subiteration_sampled(C, name):
     assert rel(gg_gpu.ravel()[idx], go) <= 1e-4, rel(gg_gpu.ravel()[idx], go)
     hto = dl32.ravel()[idx] * xo.ravel()[idx] - ho
     assert rel(ht_gpu.ravel()[idx], hto) <= 1e-4, rel(ht_gpu.ravel()[idx], hto)
+
+
+def test_nccl_sharded_path_world1_matches_single_gpu(C):
+    """The view-sharded solve path (partial zeta -> ncclAllReduce -> g/htilde
+    kernel) on a world-1 NCCL communicator equals the fused single-GPU path."""
+    from paper_1512_04564_b200.recon import Recon
+    pb = synthetic_problem(tiny("helical_arc"), M=3)
+    uid = C.ct_nccl_unique_id()
+    d = C.ct_dist_create(0, 1, uid, 0)
+    try:
+        outs = []
+        for dist in (None, d):
+            r = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], dist=dist)
+            r.compute_DL()
+            r.run(7)
+            outs.append((host(r.x), host(r.g), host(r.htilde), host(r.dl)))
+            r.close()
+        for a, b in zip(*outs):
+            assert rel(b, a) <= 1e-5   # same arithmetic, different FMA contraction
+    finally:
+        C.ct_dist_destroy(d)
