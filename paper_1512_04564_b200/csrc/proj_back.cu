@@ -16,16 +16,18 @@
 //   BK_INIT    zeta = M A'r;  g = zeta; htilde = zeta         (line 1)
 //   BK_UPDATE  zeta = M A'r;  g = rho/(rho+1)(alpha zeta + (1-alpha) g) + g/(rho+1);
 //              htilde += alpha zeta                            (lines 6-8)
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace ctr {
 
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ = 16;
-constexpr int BK_RMAX = 48;  // rows buffered per pass (more rows => several passes)
+constexpr int BK_KZ_DEFAULT = 16;  // voxels per thread in z (tuning knob CTR_BK_KZ = 16 | 24 | 32)
+constexpr int BK_RMAX = 40;  // rows buffered per pass (more rows => several passes)
 
-template <bool ARC, int DIM, int EPI, bool LZ>
+template <bool ARC, int DIM, int EPI, bool LZ, int BK_KZ>
 __global__ void __launch_bounds__(BK_BS)
 k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
@@ -150,26 +152,48 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 }
 
+template <bool ARC, int DIM, int KZ>
+static void back_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
+                             float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
+    dim3 block(32, BK_Y);
+    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, DIM == 3 ? (G.nz + KZ - 1) / KZ : 1);
+    switch (epi) {
+        case BK_WRITE:
+            if (lz) k_back<ARC, DIM, BK_WRITE, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back<ARC, DIM, BK_WRITE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_ACCUM:
+            if (lz) k_back<ARC, DIM, BK_ACCUM, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back<ARC, DIM, BK_ACCUM, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_INIT:
+            k_back<ARC, DIM, BK_INIT, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        default:
+            k_back<ARC, DIM, BK_UPDATE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+    }
+}
+
+static int back_kz() {
+    static int kz = [] {
+        const char* e = getenv("CTR_BK_KZ");
+        const int v = e ? atoi(e) : BK_KZ_DEFAULT;
+        return (v == 8 || v == 12 || v == 24 || v == 32) ? v : 16;
+    }();
+    return kz;
+}
+
 template <bool ARC, int DIM>
 static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
                           float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
-    dim3 block(32, BK_Y);
-    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, DIM == 3 ? (G.nz + BK_KZ - 1) / BK_KZ : 1);
-    switch (epi) {
-        case BK_WRITE:
-            if (lz) k_back<ARC, DIM, BK_WRITE, true><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back<ARC, DIM, BK_WRITE, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        case BK_ACCUM:
-            if (lz) k_back<ARC, DIM, BK_ACCUM, true><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back<ARC, DIM, BK_ACCUM, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        case BK_INIT:
-            k_back<ARC, DIM, BK_INIT, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        default:
-            k_back<ARC, DIM, BK_UPDATE, false><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
+    if (DIM != 3) return back_dispatch_kz<ARC, DIM, 1>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s);
+    switch (back_kz()) {
+        case 8: back_dispatch_kz<ARC, DIM, 8>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 12: back_dispatch_kz<ARC, DIM, 12>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 24: back_dispatch_kz<ARC, DIM, 24>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 32: back_dispatch_kz<ARC, DIM, 32>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        default: back_dispatch_kz<ARC, DIM, 16>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
     }
 }
 
