@@ -95,66 +95,68 @@ def sample_ellipsoids(geom, n_ellipsoids, seed, max_tries=1000):
 def voxelize(geom, ells, sub=None, device="cpu"):
     """Voxel averages of the phantom with sub^d sub-samples per voxel.
 
-    Returns a float64 tensor (nz, ny, nx) (nz = 1 in 2-D)."""
+    Returns a float64 tensor (nz, ny, nx) (nz = 1 in 2-D).  Vectorised over
+    ellipsoids and blocks of z-slices."""
     three_d = geom["dim"] == 3
     if sub is None:
         sub = 4 if not three_d else 2
     nx, ny, nz = geom["nx"], geom["ny"], geom["nz"] if three_d else 1
     dx, dy, dz = geom["dx"], geom["dy"], geom["dz"]
     f = torch.float64
+    e = torch.as_tensor(np.asarray(ells, dtype=np.float64), device=device)
+    cx, cy, cz, ax, ay, az, ang, dens = e.unbind(1)
+    c, s = torch.cos(ang), torch.sin(ang)
     xc = (torch.arange(nx, dtype=f, device=device) - (nx - 1) / 2) * dx + geom["offset_x"]
     yc = (torch.arange(ny, dtype=f, device=device) - (ny - 1) / 2) * dy + geom["offset_y"]
     zc = (torch.arange(nz, dtype=f, device=device) - (nz - 1) / 2) * dz + geom["offset_z"]
-    offs = (torch.arange(sub, dtype=f, device=device) + 0.5) / sub - 0.5
+    offs = [((i + 0.5) / sub - 0.5) for i in range(sub)]
+    zoffs = offs if three_d else [0.0]
     out = torch.zeros((nz, ny, nx), dtype=f, device=device)
-    zsubs = offs if three_d else torch.zeros(1, dtype=f, device=device)
-    for k in range(nz):
-        acc = torch.zeros((ny, nx), dtype=f, device=device)
-        for oz_ in zsubs:
-            z = zc[k] + oz_ * dz
+    zb = max(1, int(32e6 // max(1, ny * nx * len(ells))))
+    for k0 in range(0, nz, zb):
+        k1 = min(nz, k0 + zb)
+        acc = torch.zeros((k1 - k0, ny, nx), dtype=f, device=device)
+        for oz_ in zoffs:
+            Z = (zc[k0:k1] + oz_ * dz)[:, None, None, None]
             for oy_ in offs:
-                Y = (yc + oy_ * dy)[:, None]
+                Y = (yc + oy_ * dy)[None, :, None, None]
                 for ox_ in offs:
-                    X = (xc + ox_ * dx)[None, :]
-                    for e in ells:
-                        cx, cy, cz, ax, ay, az, ang, dens = [float(v) for v in e]
-                        c, s = math.cos(ang), math.sin(ang)
-                        u = (X - cx) * c + (Y - cy) * s
-                        v = -(X - cx) * s + (Y - cy) * c
-                        r = (u / ax) ** 2 + (v / ay) ** 2
-                        if three_d:
-                            r = r + ((z - cz) / az) ** 2
-                        acc += dens * (r <= 1.0).to(f)
-        out[k] = acc / (sub ** (3 if three_d else 2))
+                    X = (xc + ox_ * dx)[None, None, :, None]
+                    u = (X - cx) * c + (Y - cy) * s
+                    v = -(X - cx) * s + (Y - cy) * c
+                    r = (u / ax) ** 2 + (v / ay) ** 2
+                    if three_d:
+                        r = r + ((Z - cz) / az) ** 2
+                    acc += ((r <= 1.0).to(f) * dens).sum(-1)
+        out[k0:k1] = acc / (sub ** (3 if three_d else 2))
     return out
 
 
 def line_integrals(ells, P, D, three_d):
     """Sum of ellipsoid chords along rays P + lambda*D (|D| = 1), SURVEY 8c.5.
 
-    P, D: (..., 3) float64 tensors.  Returns (...) float64."""
-    out = torch.zeros(P.shape[:-1], dtype=P.dtype, device=P.device)
-    for e in ells:
-        cx, cy, cz, ax, ay, az, ang, dens = [float(v) for v in e]
-        c, s = math.cos(ang), math.sin(ang)
-        px, py, pz = P[..., 0] - cx, P[..., 1] - cy, P[..., 2] - cz
-        # R^T (p - c), then scale by 1/a
-        pu = (px * c + py * s) / ax
-        pv = (-px * s + py * c) / ay
-        du = (D[..., 0] * c + D[..., 1] * s) / ax
-        dv = (-D[..., 0] * s + D[..., 1] * c) / ay
-        if three_d:
-            pw = pz / az
-            dw = D[..., 2] / az
-        else:
-            pw = torch.zeros_like(pu)
-            dw = torch.zeros_like(du)
-        dd = du * du + dv * dv + dw * dw
-        pd = pu * du + pv * dv + pw * dw
-        pp = pu * pu + pv * pv + pw * pw
-        disc = pd * pd - dd * (pp - 1.0)
-        out += dens * 2.0 * torch.sqrt(torch.clamp(disc, min=0.0)) / dd
-    return out
+    P, D: (..., 3) float64 tensors.  Returns (...) float64.  Vectorised over
+    the ellipsoids (one set of tensor ops for all of them)."""
+    e = torch.as_tensor(np.asarray(ells, dtype=np.float64), device=P.device)
+    cx, cy, cz, ax, ay, az, ang, dens = e.unbind(1)
+    c, s = torch.cos(ang), torch.sin(ang)
+    px = P[..., 0:1] - cx
+    py = P[..., 1:2] - cy
+    pu = (px * c + py * s) / ax
+    pv = (-px * s + py * c) / ay
+    du = (D[..., 0:1] * c + D[..., 1:2] * s) / ax
+    dv = (-D[..., 0:1] * s + D[..., 1:2] * c) / ay
+    dd = du * du + dv * dv
+    pd = pu * du + pv * dv
+    pp = pu * pu + pv * pv
+    if three_d:
+        pw = (P[..., 2:3] - cz) / az
+        dw = D[..., 2:3] / az
+        dd = dd + dw * dw
+        pd = pd + pw * dw
+        pp = pp + pw * pw
+    disc = pd * pd - dd * (pp - 1.0)
+    return (dens * 2.0 * torch.sqrt(torch.clamp(disc, min=0.0)) / dd).sum(-1)
 
 
 def view_angles(geom, views):
@@ -206,7 +208,7 @@ def rays(geom, views, s_pos, t_pos):
     return P, D
 
 
-def analytic_sinogram(geom, ells, views=None, sub_s=2, sub_t=2, device="cpu", chunk=16):
+def analytic_sinogram(geom, ells, views=None, sub_s=2, sub_t=2, device="cpu", chunk=None):
     """Analytic line integrals averaged over sub_s x sub_t sub-rays per cell.
 
     Returns float64 (V, nt, ns) (nt = 1 in 2-D)."""
@@ -223,6 +225,8 @@ def analytic_sinogram(geom, ells, views=None, sub_s=2, sub_t=2, device="cpu", ch
     scol = torch.arange(ns, dtype=f, device=device)
     trow = torch.arange(nt, dtype=f, device=device)
     out = torch.zeros((views.numel(), nt, ns), dtype=f, device=device)
+    if chunk is None:   # keep the (views, rows, cols, ellipsoids) temporaries near 64 M elements
+        chunk = max(1, int(64e6 // max(1, nt * ns * len(ells))))
     for v0 in range(0, views.numel(), chunk):
         vv = views[v0:v0 + chunk]
         acc = torch.zeros((vv.numel(), nt, ns), dtype=f, device=device)
