@@ -108,6 +108,8 @@ static ct_status validate_desc(const ct_geom_desc* d) {
         return fail(CT_E_CONFIG, "non-finite orbit parameters");
     if ((long long)d->nx * d->ny * d->nz > (1LL << 33)) return fail(CT_E_CONFIG, "volume too large");
     if (d->nt > 128) return fail(CT_E_CONFIG, "nt = %d > 128 detector rows", d->nt);
+    // the update kernel keeps x+ of a 32-column tile in shared memory for the z-prefix
+    if (d->nz > 1536) return fail(CT_E_CONFIG, "nz = %d > 1536 slices", d->nz);
     // source must stay outside the volume's circumscribed cylinder
     const double ex = 0.5 * d->nx * d->dx + std::fabs(d->offset_x);
     const double ey = 0.5 * d->ny * d->dy + std::fabs(d->offset_y);
@@ -313,7 +315,7 @@ static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dis
     L.xalt = off;
     off = align_up(off + sizeof(float) * g->G.nvox);
     L.xt = off;  // z-prefix array of x+ for the 3-D forward projector
-    if (g->G.dim == 3) off = align_up(off + sizeof(float) * (size_t)g->G.nxy * pfx_stride_of(g->G));
+    if (g->G.dim == 3) off = align_up(off + sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G));
     L.r = off;
     off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
     L.zeta = off;

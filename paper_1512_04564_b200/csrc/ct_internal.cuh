@@ -73,6 +73,15 @@ __device__ __forceinline__ Views select_views(const Ctl* c, Views v) {
     return o;
 }
 
+// MUFU.RSQ without the denormal fix-up rsqrtf() carries (3 extra instructions):
+// every call site passes an argument >= 1 (potential weights) or a squared
+// distance of millimetres (footprints), never a denormal.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ void sort4(float& a, float& b, float& c, float& d) {
     float t;
 #define CTR_CS(p, q) if (p > q) { t = p; p = q; q = t; }
@@ -95,38 +104,65 @@ struct Footprint {
 // O(voxel) quantities, computed as atan(z) ~ z - z^3/3 + z^5/5 of z = cross/dot
 // (|z| < 0.05 in every supported geometry: truncation < 1e-8 relative) and
 // with fast reciprocals (__fdividef, rsqrtf: 2 ulp) -- DESIGN.md §5.
-template <bool ARC>
-__device__ __forceinline__ void ct_footprint(const DGeom& G, float cb, float sb, float zs, int i, int j,
-                                             Footprint& f) {
+//
+// The footprint is evaluated in three parts so that the back-projector can
+// test the cheap axial extent before paying for the transaxial corners:
+// fp_base (source-to-column vector in the view frame), fp_axial (B0, H) and
+// fp_trans (corner taus, ramps, L_xy).  ct_footprint = all three; every caller
+// (forward, back, nnz count) runs the same expressions.
+struct FpBase {
+    float rx, ry;     // column centre - source (world xy)
+    float a, b;       // the same in the view frame (e_c, e_u)
+    float r2, rinv;   // |r|^2, 1/|r|
+    float inva;       // 1/a
+};
+
+__device__ __forceinline__ void fp_base(const DGeom& G, float cb, float sb, int i, int j, FpBase& q) {
     const float cx = fmaf((float)i, G.dx, G.x0);
     const float cy = fmaf((float)j, G.dy, G.y0);
-    const float rx = fmaf(-G.dso, cb, cx);
-    const float ry = fmaf(-G.dso, sb, cy);
+    q.rx = fmaf(-G.dso, cb, cx);
+    q.ry = fmaf(-G.dso, sb, cy);
     // frame of the view: a along e_c = -(cos,sin), b along e_u = (-sin, cos)
-    const float a = -(rx * cb + ry * sb);
-    const float b = ry * cb - rx * sb;
+    q.a = -(q.rx * cb + q.ry * sb);
+    q.b = q.ry * cb - q.rx * sb;
+    q.r2 = fmaf(q.a, q.a, q.b * q.b);
+    q.rinv = rsqrt_ftz(q.r2);
+    q.inva = __fdividef(1.f, q.a);
+}
+
+// axial magnification: flat Dsd/a, arc Dsd/|r|; row units u = t/dt + t_c0p;
+// voxel k spans row units [B0 + k H, B0 + (k+1) H]
+template <bool ARC>
+__device__ __forceinline__ void fp_axial(const DGeom& G, const FpBase& q, float zs, float& B0, float& H) {
+    const float mag = ARC ? G.dsd * q.rinv : G.dsd * q.inva;
+    const float mdt = mag * G.inv_dt;
+    H = G.dz * mdt;
+    B0 = fmaf(G.z0 - 0.5f * G.dz - zs, mdt, G.t_c0p);
+}
+
+template <bool ARC>
+__device__ __forceinline__ void fp_trans(const DGeom& G, float cb, float sb, const FpBase& q, Footprint& f) {
+    const float a = q.a, b = q.b;
     const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
     // corner offsets (+-hx, +-hy) in (a, b): da = -(ex cb + ey sb), db = ey cb - ex sb
     const float da1 = hx * cb, da2 = hy * sb;
     const float db1 = hx * sb, db2 = hy * cb;
-    const float r2 = fmaf(a, a, b * b);
-    const float inva = __fdividef(1.f, a);
     float t[4];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-        const float sx = (q & 1) ? 1.f : -1.f;
-        const float sy = (q & 2) ? 1.f : -1.f;
+    for (int c = 0; c < 4; c++) {
+        const float sx = (c & 1) ? 1.f : -1.f;
+        const float sy = (c & 2) ? 1.f : -1.f;
         const float dA = -(sx * da1 + sy * da2);
         const float dB = sy * db2 - sx * db1;
         const float cr = a * dB - b * dA;
         if (ARC) {
             // angle(p_k) - angle(p_c) = atan(cr / (a (a + da) + b (b + db)))
-            const float z = __fdividef(cr, r2 + fmaf(a, dA, b * dB));
+            const float z = __fdividef(cr, q.r2 + fmaf(a, dA, b * dB));
             const float z2 = z * z;
-            t[q] = z * fmaf(z2, fmaf(z2, 0.2f, -0.33333334f), 1.f);
+            t[c] = z * fmaf(z2, fmaf(z2, 0.2f, -0.33333334f), 1.f);
         } else {
             // Dsd (b+db)/(a+da) - Dsd b/a = Dsd (db a - b da) / (a (a + da))
-            t[q] = G.dsd * cr * inva * __fdividef(1.f, a + dA);
+            t[c] = G.dsd * cr * q.inva * __fdividef(1.f, a + dA);
         }
     }
     const float tc = ARC ? atan2f(b, a) : G.dsd * b / a;
@@ -141,17 +177,20 @@ __device__ __forceinline__ void ct_footprint(const DGeom& G, float cb, float sb,
     f.halfr2 = w2 > kRampEps ? 0.5f * w2 : 0.f;
     f.inv2r2 = w2 > kRampEps ? __fdividef(0.5f, w2) : 0.f;
     // L_xy = min(dx/|d_x|, dy/|d_y|) with d = (rx, ry)/|r|, |r| = |(a, b)|
-    const float rinv = rsqrtf(r2);
-    const float rn = r2 * rinv;
-    const float arx = fabsf(rx), ary = fabsf(ry);
+    const float rn = q.r2 * q.rinv;
+    const float arx = fabsf(q.rx), ary = fabsf(q.ry);
     const float lx = arx > 0.f ? __fdividef(G.dx * rn, arx) : 3.0e38f;
     const float ly = ary > 0.f ? __fdividef(G.dy * rn, ary) : 3.0e38f;
     f.lxy = fminf(lx, ly);
-    // axial magnification: flat Dsd/a, arc Dsd/|r|; row units u = t/dt + t_c0p
-    const float mag = ARC ? G.dsd * rinv : G.dsd * inva;
-    const float mdt = mag * G.inv_dt;
-    f.H = G.dz * mdt;
-    f.B0 = fmaf(G.z0 - 0.5f * G.dz - zs, mdt, G.t_c0p);
+}
+
+template <bool ARC>
+__device__ __forceinline__ void ct_footprint(const DGeom& G, float cb, float sb, float zs, int i, int j,
+                                             Footprint& f) {
+    FpBase q;
+    fp_base(G, cb, sb, i, j, q);
+    fp_trans<ARC>(G, cb, sb, q, f);
+    fp_axial<ARC>(G, q, zs, f.B0, f.H);
 }
 
 // Antiderivative of the unit-height trapezoid at column-relative coordinate u

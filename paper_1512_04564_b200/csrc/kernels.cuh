@@ -17,10 +17,12 @@ struct RegParams {
 // by this sub-iteration's update (parity of k - k_base), else xa.
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
                 const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
-                int pfx_stride = 0);  // > 0: xa is the z-prefix array (3-D solve path)
+                int pfx_stride = 0);  // > 0: xa is the float2 z-prefix array (3-D solve path)
 
-// column stride (floats) of the z-prefix array P_0..P_nz, P_nz+1 (= P_nz): nz + 2 rounded up to 4
-__host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 2) + 3) & ~3; }
+// z-prefix array of x+ for the 3-D forward (written by the update kernel):
+// per voxel column, float2 Q_k = (P_k, x_k) for k = 0..nz-1 and Q_nz = (P_nz, 0),
+// P_k = sum_{k'<k} x_k'.  Column stride in float2 units: nz + 1 rounded up to even.
+__host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 1) + 1) & ~1; }
 
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);

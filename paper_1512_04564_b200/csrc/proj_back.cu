@@ -1,15 +1,12 @@
 // proj_back.cu — K3 (+K5 epilogue): voxel-driven separable-footprint
 // back-projection, a gather over the subset's views.
 //
-// Thread = one voxel column (i, j) and a z-chunk of BK_KZ voxels (register
-// accumulators); block = 32 x BK_Y columns (32 consecutive x in a warp, so a
-// warp's sinogram reads hit consecutive detector columns).  Per view the
-// thread evaluates the column's footprint once (ct_footprint, shared with the
-// forward kernel), keeps F1 of its <= kMaxCells columns in a per-thread
-// shared-memory slot, forms the row sums rs(t) = L_xy sum_s F1(s) r[t][s] of
-// the rows its chunk projects to, then distributes them to its voxels with
-// the exact overlaps F2, evaluated as differences of the cumulative row sum
-// at the voxel boundaries b_k = B0 + k H (one interpolation per voxel).
+// 3-D (k_back3): thread = one voxel column (i, j) x a z-chunk of BK_KZ voxels
+// (register accumulators); block = 32 x BK_Y columns (32 consecutive x in a
+// warp, so a warp's sinogram reads hit neighbouring detector columns).  The
+// kernel comment below gives the per-view steps.  2-D (k_back2): thread = one
+// pixel.  Both evaluate the footprint with the functions the forward uses
+// (ct_internal.cuh), so A' is the transpose of A up to rounding.
 //
 // Epilogues (Algorithm 1; htilde form):
 //   BK_WRITE   out = scale * A'r          BK_ACCUM out += scale * A'r
@@ -24,24 +21,86 @@ namespace ctr {
 
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ_DEFAULT = 16;  // voxels per thread in z (tuning knob CTR_BK_KZ = 16 | 24 | 32)
-constexpr int BK_RMAX = 40;  // rows buffered per pass (more rows => several passes)
+constexpr int BK_KZ_DEFAULT = 16;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24)
+constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 (more rows => several passes)
 
-template <bool ARC, int DIM, int EPI, bool LZ, int BK_KZ>
+// 2-D back-projection: thread = one pixel; per view one footprint and the
+// F1-weighted sum over the <= kMaxCells cells it covers.
+template <bool ARC, int EPI>
 __global__ void __launch_bounds__(BK_BS)
-k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
-       const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
-       float* __restrict__ htbuf) {
-    __shared__ float f1s[kMaxCells][BK_BS];
-    __shared__ float csb[(DIM == 3) ? BK_RMAX + 2 : 1][BK_BS];
+k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+        const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
+        float* __restrict__ htbuf) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * BK_Y + threadIdx.y;
+    if (i >= G.nx || j >= G.ny) return;
+    const Views V = select_views(ctl, vsel);
+    float acc = 0.f;
+    for (int vi = 0; vi < V.count; vi++) {
+        const int v = V.start + vi * V.stride;
+        const float4 vw = __ldg(&vtab[v]);
+        Footprint f;
+        ct_footprint<ARC>(G, vw.x, vw.y, vw.z, i, j, f);
+        const int slo = max((int)floorf(f.sfc + f.u0 + 0.5f), 0);
+        const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), G.ns - 1);
+        const float* __restrict__ pr = proj + (size_t)vi * G.ns;
+        float Tprev = trap_T(f, ((float)slo - 0.5f) - f.sfc);
+        float rs = 0.f;
+        for (int s = slo; s <= shi; s++) {
+            const float Tn = trap_T(f, ((float)s + 0.5f) - f.sfc);
+            rs = fmaf(Tn - Tprev, __ldg(pr + s), rs);
+            Tprev = Tn;
+        }
+        acc = fmaf(f.lxy, rs, acc);
+    }
+    const size_t idx = (size_t)j * G.nx + i;
+    const float z = scale * acc;
+    if (EPI == BK_WRITE) {
+        out[idx] = z;
+    } else if (EPI == BK_ACCUM) {
+        out[idx] += z;
+    } else if (EPI == BK_INIT) {
+        gbuf[idx] = z;
+        htbuf[idx] = z;
+    } else {
+        const float rho = rho_of_k(ctl), alpha = ctl->alpha;
+        const float gv = gbuf[idx];
+        const float inv = 1.f / (rho + 1.f);
+        gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
+        htbuf[idx] = fmaf(alpha, z, htbuf[idx]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// 3-D back-projection.  Thread = one voxel column (i, j) x a z-chunk of BK_KZ
+// voxels; block = 32 x BK_Y columns.  Per view:
+//   1. axial extent first (fp_base + fp_axial: ~20 instructions): a chunk
+//      whose rows [B0 + k0 H, B0 + (k0+kz) H] miss the detector skips the view
+//      (helical views see a z-band only);
+//   2. transaxial footprint (fp_trans) and F1 of the <= 4 detector columns it
+//      covers, kept in registers (wider footprints take a general loop);
+//   3. per row t: rs(t) = L_xy sum_s F1(s) r[t][s] (4 gathers + 4 FMA), stored
+//      with its running sum as float2 (cs_t, rs_t) in a per-thread
+//      shared-memory column;
+//   4. per voxel: the F2-weighted row sum is R(b_k+1) - R(b_k) with the
+//      piecewise-linear cumulative R(u) = cs_o + frac rs_o (one 8-byte shared
+//      load per voxel boundary, magic-number floor).
+template <bool ARC, int EPI, bool LZ, int BK_KZ>
+__global__ void __launch_bounds__(BK_BS, 7)
+k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+        const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
+        float* __restrict__ htbuf) {
+    constexpr int RM = BK_RMAX3;
+    __shared__ float2 csb[RM + 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
     const int k0 = blockIdx.z * BK_KZ;
     if (i >= G.nx || j >= G.ny) return;
     const Views V = select_views(ctl, vsel);
-    const int nt = (DIM == 3) ? G.nt : 1;
-    const int kz = (DIM == 3) ? min(BK_KZ, G.nz - k0) : 1;
+    const int nt = G.nt;
+    const float fkz = (float)min(BK_KZ, G.nz - k0);
+    float2* __restrict__ cs = &csb[0][tid];
 
     float acc[BK_KZ];
 #pragma unroll
@@ -50,76 +109,97 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     for (int vi = 0; vi < V.count; vi++) {
         const int v = V.start + vi * V.stride;
         const float4 vw = __ldg(&vtab[v]);
+        FpBase fb;
+        fp_base(G, vw.x, vw.y, i, j, fb);
+        float B0, H;
+        fp_axial<ARC>(G, fb, vw.z, B0, H);
+        const float clo = fmaf((float)k0, H, B0);
+        const float chi = fmaf(fkz, H, clo);
+        const int t0 = max((int)floorf(clo), 0);
+        const int t1 = min((int)ceilf(chi), nt) - 1;
+        if (t0 > t1) continue;
         Footprint f;
-        ct_footprint<ARC>(G, vw.x, vw.y, vw.z, i, j, f);
-        int t0 = 0, t1 = 0;
-        if (DIM == 3) {
-            const float clo = voxel_b(f, k0), chi = voxel_b(f, k0 + kz);
-            t0 = max((int)floorf(clo), 0);
-            t1 = min((int)ceilf(chi), nt) - 1;
-            if (t0 > t1) continue;
-        }
+        fp_trans<ARC>(G, vw.x, vw.y, fb, f);
         // detector columns under the footprint
-        int slo = (int)floorf(f.sfc + f.u0 + 0.5f);
-        int shi = (int)floorf(f.sfc + f.u3 + 0.5f);
-        slo = max(slo, 0);
-        shi = min(shi, G.ns - 1);
-        int nc = shi - slo + 1;
+        const int slo = max((int)floorf(f.sfc + f.u0 + 0.5f), 0);
+        const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), G.ns - 1);
+        const int nc = shi - slo + 1;
         if (nc <= 0) continue;
-        if (nc > kMaxCells) nc = kMaxCells;  // excluded at ct_geom_create (footprint bound)
+        const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
+        // 4-column window [sw, sw + 3] inside the detector; F1 is exactly 0 outside [u0, u3]
+        const int sw = nc <= 4 ? max(min(slo, G.ns - 4), 0) : slo;
+        float F[4];
         {
-            float Tprev = trap_T(f, ((float)slo - 0.5f) - f.sfc);
-            for (int q = 0; q < nc; q++) {
-                const float Tn = trap_T(f, ((float)(slo + q) + 0.5f) - f.sfc);
-                f1s[q][tid] = (Tn - Tprev) * f.lxy;
+            float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
+                F[q] = (Tn - Tprev) * f.lxy;
                 Tprev = Tn;
             }
         }
-        const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns + (unsigned)slo;  // < 2^32 (checked at launch)
-        if (DIM != 3) {
-            float rs = 0.f;
-            for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(proj + (pv + q)), rs);
-            acc[0] += rs;
-            continue;
-        }
-        for (int tw = t0; tw <= t1; tw += BK_RMAX) {
-            const int twe = min(t1, tw + BK_RMAX - 1);
-            // row sums rs(t) -> running sums cs[o] = sum_{tw <= t < tw+o} rs(t) (cs[n+1] = cs[n]
-            // pads the top).  The F2-weighted sum over the rows of voxel k is R(b_k+1) - R(b_k)
-            // with the piecewise-linear cumulative R(u) = cs[o] + frac (cs[o+1] - cs[o]).
+        const float Bs = B0 - 0.5f;  // voxel boundary in row units minus (row + 1/2) below
+        for (int tw = t0; tw <= t1; tw += RM) {
+            const int twe = min(t1, tw + RM - 1);
             const int n = twe - tw + 1;
             float run = 0.f;
-            csb[0][tid] = 0.f;
-            for (int t = tw; t <= twe; t++) {
-                const float* __restrict__ pr = proj + (pv + (unsigned)t * (unsigned)G.ns);
-                float rs = 0.f;
-                if (LZ) {
-                    for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid] * ray_Lz<ARC>(G, slo + q, t), __ldg(&pr[q]), rs);
-                } else {
-                    for (int q = 0; q < nc; q++) rs = fmaf(f1s[q][tid], __ldg(&pr[q]), rs);
+            const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns);
+            if (nc <= 4 && G.ns >= 4) {
+                pr += sw;
+                for (int o = 0; o < n; o++) {
+                    float rs;
+                    if (LZ) {
+                        const int t = tw + o;
+                        rs = F[0] * ray_Lz<ARC>(G, sw, t) * __ldg(pr);
+                        rs = fmaf(F[1] * ray_Lz<ARC>(G, sw + 1, t), __ldg(pr + 1), rs);
+                        rs = fmaf(F[2] * ray_Lz<ARC>(G, sw + 2, t), __ldg(pr + 2), rs);
+                        rs = fmaf(F[3] * ray_Lz<ARC>(G, sw + 3, t), __ldg(pr + 3), rs);
+                    } else {
+                        rs = F[0] * __ldg(pr);
+                        rs = fmaf(F[1], __ldg(pr + 1), rs);
+                        rs = fmaf(F[2], __ldg(pr + 2), rs);
+                        rs = fmaf(F[3], __ldg(pr + 3), rs);
+                    }
+                    cs[o * BK_BS] = make_float2(run, rs);
+                    run += rs;
+                    pr += G.ns;
                 }
-                run += rs;
-                csb[t - tw + 1][tid] = run;
+            } else {
+                // wide footprint (near the source in steep geometries): F1 on the fly
+                for (int o = 0; o < n; o++) {
+                    const int t = tw + o;
+                    float rs = 0.f;
+                    float Tprev = trap_T(f, ((float)slo - 0.5f) - f.sfc);
+                    for (int q = 0; q < nc; q++) {
+                        const float Tn = trap_T(f, ((float)(slo + q) + 0.5f) - f.sfc);
+                        const float wq = LZ ? (Tn - Tprev) * f.lxy * ray_Lz<ARC>(G, slo + q, t) : (Tn - Tprev) * f.lxy;
+                        rs = fmaf(wq, __ldg(pr + slo + q), rs);
+                        Tprev = Tn;
+                    }
+                    cs[o * BK_BS] = make_float2(run, rs);
+                    run += rs;
+                    pr += G.ns;
+                }
             }
-            csb[n + 1][tid] = run;
-            const float shift = (float)tw + 0.5f, vmax = (float)n - 0.5f;
-            auto R = [&](float u) {
-                // o = round(v - 1/2), v = u - tw in [0, n]: o <= v <= o + 1 (magic-number floor)
-                const float vv = fminf(fmaxf(u - shift, -0.5f), vmax);
+            cs[n * BK_BS] = make_float2(run, 0.f);
+            // R(u) at voxel boundary u = B0 + k H: v = u - (tw + 1/2) in [-1/2, n - 1/2],
+            // o = round(v) (magic number), frac = v + 1/2 - o in [0, 1]
+            const float sh = Bs - (float)tw;
+            const float vmax = (float)n - 0.5f;
+            auto R = [&](int k) {
+                const float vv = fminf(fmaxf(fmaf((float)k, H, sh), -0.5f), vmax);
                 const float rm = __fadd_rn(vv, 12582912.0f);
                 const int o = __float_as_int(rm) - 0x4B400000;
                 const float fr = (vv + 0.5f) - (rm - 12582912.0f);
-                const float c0 = csb[o][tid];
-                return fmaf(fr, csb[o + 1][tid] - c0, c0);
+                const float2 c = cs[o * BK_BS];
+                return fmaf(fr, c.y, c.x);
             };
-            float Rlo = R(voxel_b(f, k0));
+            float Rlo = R(k0);
 #pragma unroll
             for (int q = 0; q < BK_KZ; q++) {
-                if (q < kz) {
-                    const float Rhi = R(voxel_b(f, k0 + q + 1));
-                    acc[q] += Rhi - Rlo;
-                    Rlo = Rhi;
-                }
+                const float Rhi = R(k0 + q + 1);
+                acc[q] += Rhi - Rlo;
+                Rlo = Rhi;
             }
         }
     }
@@ -130,6 +210,7 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         rho = rho_of_k(ctl);
         alpha = ctl->alpha;
     }
+    const int kz = min(BK_KZ, G.nz - k0);
 #pragma unroll
     for (int q = 0; q < BK_KZ; q++) {
         if (q < kz) {
@@ -152,26 +233,39 @@ k_back(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 }
 
-template <bool ARC, int DIM, int KZ>
-static void back_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
-                             float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
+template <bool ARC, int KZ>
+static void back3_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
+                              float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
     dim3 block(32, BK_Y);
-    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, DIM == 3 ? (G.nz + KZ - 1) / KZ : 1);
+    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, (G.nz + KZ - 1) / KZ);
     switch (epi) {
         case BK_WRITE:
-            if (lz) k_back<ARC, DIM, BK_WRITE, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back<ARC, DIM, BK_WRITE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            if (lz) k_back3<ARC, BK_WRITE, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back3<ARC, BK_WRITE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         case BK_ACCUM:
-            if (lz) k_back<ARC, DIM, BK_ACCUM, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back<ARC, DIM, BK_ACCUM, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            if (lz) k_back3<ARC, BK_ACCUM, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back3<ARC, BK_ACCUM, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         case BK_INIT:
-            k_back<ARC, DIM, BK_INIT, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            k_back3<ARC, BK_INIT, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         default:
-            k_back<ARC, DIM, BK_UPDATE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            k_back3<ARC, BK_UPDATE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
+    }
+}
+
+template <bool ARC>
+static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
+                           float scale, int epi, float* out, float* g, float* ht, cudaStream_t s) {
+    dim3 block(32, BK_Y);
+    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, 1);
+    switch (epi) {
+        case BK_WRITE: k_back2<ARC, BK_WRITE><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_ACCUM: k_back2<ARC, BK_ACCUM><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_INIT: k_back2<ARC, BK_INIT><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        default: k_back2<ARC, BK_UPDATE><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
     }
 }
 
@@ -179,7 +273,7 @@ static int back_kz() {
     static int kz = [] {
         const char* e = getenv("CTR_BK_KZ");
         const int v = e ? atoi(e) : BK_KZ_DEFAULT;
-        return (v == 8 || v == 12 || v == 24 || v == 32) ? v : 16;
+        return (v == 8 || v == 24) ? v : 16;
     }();
     return kz;
 }
@@ -187,13 +281,11 @@ static int back_kz() {
 template <bool ARC, int DIM>
 static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
                           float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
-    if (DIM != 3) return back_dispatch_kz<ARC, DIM, 1>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s);
+    if (DIM != 3) return back2_dispatch<ARC>(G, vtab, ctl, v, proj, scale, epi, out, g, ht, s);
     switch (back_kz()) {
-        case 8: back_dispatch_kz<ARC, DIM, 8>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        case 12: back_dispatch_kz<ARC, DIM, 12>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        case 24: back_dispatch_kz<ARC, DIM, 24>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        case 32: back_dispatch_kz<ARC, DIM, 32>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        default: back_dispatch_kz<ARC, DIM, 16>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 8: back3_dispatch_kz<ARC, 8>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 24: back3_dispatch_kz<ARC, 24>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        default: back3_dispatch_kz<ARC, 16>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
     }
 }
 

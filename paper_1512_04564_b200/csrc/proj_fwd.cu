@@ -1,17 +1,10 @@
 // proj_fwd.cu — K1+K2: ray-driven separable-footprint forward projection with
 // the statistically weighted residual fused in the epilogue.
 //
-// One thread owns one detector column s of one view (a "cell" in 2-D, a
-// column of nt rows in 3-D); a block owns FWD_BS consecutive columns of one
-// view.  The thread walks the fan wedge of its column along the dominant
-// axis of its central ray, tests each candidate voxel column against the two
-// edge rays (support-function test of the square against the two
-// half-planes), evaluates the SF footprint of the surviving columns
-// (ct_footprint, the same function the back-projector uses) and, in 3-D,
-// resamples the voxel column onto the detector rows by a merge of the voxel
-// and row boundaries (exact overlaps, F2).  Row sums accumulate in a
-// per-thread shared-memory column acc[t][tid]: a gather — no atomics, no
-// cross-thread writes, no __syncthreads.
+// Gathers over the fan wedge of a group of detector columns (2-D: k_fwd2,
+// 3-D: k_fwd3, described at each kernel); both test candidate voxel columns
+// against the wedge's edge rays and evaluate the SF footprint with
+// ct_footprint, the function the back-projector uses.  No atomics.
 //
 // Epilogue (Eq. 36 applied implicitly):
 //   FWD_PLAIN  p = L_z q
@@ -21,38 +14,46 @@
 
 namespace ctr {
 
-constexpr int FWD_BS = 128;
+// ---------------------------------------------------------------------------
+// 2-D forward projection.  A warp owns F2_CPW = 8 adjacent detector cells
+// s0..s0+7 of one view and walks the union of their fan wedges along the
+// dominant axis, F2_SPP = 4 slabs per pass: the 8 lanes of a slab split its
+// candidate pixels (support-function test of the pixel square against the two
+// union edge rays), evaluate the SF footprint (ct_footprint, shared with the
+// back-projector), F1 of the 8 cells from 9 edge evaluations of the trapezoid
+// antiderivative, and accumulate L_xy F1 x into 8 per-lane registers.  A warp
+// reduction forms the 8 sums; no atomics, no shared memory.
+constexpr int F2_CPW = 8;
+constexpr int F2_SUB = 8;            // lanes per slab
+constexpr int F2_SPP = 32 / F2_SUB;  // slabs per pass
+constexpr int F2_WARPS = 4;
 
-template <bool ARC, int DIM, int MODE>
-__global__ void __launch_bounds__(FWD_BS)
-k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
-      const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
-      const float* __restrict__ w, float* __restrict__ out) {
-    extern __shared__ float acc[];  // [nt][FWD_BS] in 3-D
+template <bool ARC, int MODE>
+__global__ void __launch_bounds__(32 * F2_WARPS)
+k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+       const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
+       const float* __restrict__ w, float* __restrict__ out) {
+    constexpr bool ONES = (MODE == FWD_ONES_W);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const Views V = select_views(ctl, vsel);
     const int vi = blockIdx.y;
     if (vi >= V.count) return;
     const int v = V.start + vi * V.stride;
-    const int tid = threadIdx.x;
-    const int s = blockIdx.x * FWD_BS + tid;
-    if (s >= G.ns) return;
-    constexpr bool ONES = (MODE == FWD_ONES_W);
+    const int s0 = (blockIdx.x * F2_WARPS + wid) * F2_CPW;
+    if (s0 >= G.ns) return;  // warp-uniform
     const float* __restrict__ x = xa;
     if (ctl) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
-
     const float4 vw = __ldg(&vtab[v]);
-    const float cb = vw.x, sb = vw.y, zs = vw.z;
+    const float cb = vw.x, sb = vw.y;
     const float Sx = G.dso * cb, Sy = G.dso * sb;
-    const int nt = (DIM == 3) ? G.nt : 1;
-    if (DIM == 3) {
-        for (int t = 0; t < nt; t++) acc[t * FWD_BS + tid] = 0.f;
-    }
-    float q2d = 0.f;
+    float acc[F2_CPW];
+#pragma unroll
+    for (int c = 0; c < F2_CPW; c++) acc[c] = 0.f;
 
-    // edge rays of column s: tau_l, tau_r; central ray tau_m
-    const float tl = ((float)s - 0.5f - G.s_c0) * G.delta;
-    const float tr = ((float)s + 0.5f - G.s_c0) * G.delta;
-    const float tm = ((float)s - G.s_c0) * G.delta;
+    const int s7 = min(s0 + F2_CPW - 1, G.ns - 1);
+    const float tl = ((float)s0 - 0.5f - G.s_c0) * G.delta;
+    const float tr = ((float)s7 + 0.5f - G.s_c0) * G.delta;
+    const float tm = (0.5f * (float)(s0 + s7) - G.s_c0) * G.delta;
     float cal, cul, car, cur_, cam, cum;
     if (ARC) {
         sincosf(tl, &cul, &cal);
@@ -74,106 +75,73 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
     const float suppr = fabsf(nrx) * hx + fabsf(nry) * hy;
     const float tol_l = 1e-4f * suppl, tol_r = 1e-4f * suppr;
     const bool xstep = fabsf(dmx) >= fabsf(dmy);
+    const int na_ = xstep ? G.nx : G.ny, no_ = xstep ? G.ny : G.nx;
+    const float a0 = xstep ? G.x0 : G.y0, da = xstep ? G.dx : G.dy, ha = xstep ? hx : hy;
+    const float o0 = xstep ? G.y0 : G.x0, dob = xstep ? G.dy : G.dx;
+    const float Sa = xstep ? Sx : Sy, So = xstep ? Sy : Sx;
+    const float kl = xstep ? dly / dlx : dlx / dly;
+    const float kr = xstep ? dry / drx : drx / dry;
+    const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
+    const float inv_do = 1.f / dob;
 
-    auto visit = [&](int i, int j) {
-        const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
-        const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
-        if (fmaf(nlx, cx, nly * cy) + suppl < -tol_l) return;
-        if (fmaf(nrx, cx, nry * cy) + suppr < -tol_r) return;
-        Footprint f;
-        ct_footprint<ARC>(G, cb, sb, zs, i, j, f);
-        const float F1 = sf_F1(f, s);
-        if (!(F1 > 0.f)) return;
-        const float L = f.lxy * F1;
-        if (DIM != 3) {
-            q2d = fmaf(L, ONES ? 1.f : __ldg(&x[(size_t)j * G.nx + i]), q2d);
-            return;
-        }
-        // merge voxel boundaries b_k = B0 + k H with row boundaries t (row units)
-        const float ulo = fmaxf(f.B0, 0.f);
-        const float uhi = fminf(voxel_b(f, G.nz), (float)nt);
-        if (!(ulo < uhi)) return;
-        int k = (int)floorf((ulo - f.B0) / f.H);
-        k = min(max(k, 0), G.nz - 1);
-        while (k + 1 < G.nz && voxel_b(f, k + 1) <= ulo) k++;
-        while (k > 0 && voxel_b(f, k) > ulo) k--;
-        int t = min((int)floorf(ulo), nt - 1);
-        const float* __restrict__ xc = x + (size_t)j * G.nx + i;
-        float xv = ONES ? 1.f : __ldg(&xc[(size_t)k * G.nxy]);
-        float pos = ulo, cur = 0.f;
-        while (true) {
-            const float bk1 = voxel_b(f, k + 1);
-            const float tn = (float)(t + 1);
-            const float nxt = fminf(fminf(bk1, tn), uhi);
-            cur = fmaf(nxt - pos, xv, cur);
-            pos = nxt;
-            if (nxt >= uhi) break;
-            if (tn <= bk1) {
-                acc[t * FWD_BS + tid] = fmaf(L, cur, acc[t * FWD_BS + tid]);
-                cur = 0.f;
-                t++;
-            }
-            if (bk1 <= tn) {
-                k++;
-                if (!ONES) xv = __ldg(&xc[(size_t)k * G.nxy]);
+    for (int sl0 = 0; sl0 < na_; sl0 += F2_SPP) {
+        const int sl = sl0 + lane / F2_SUB, sub = lane % F2_SUB;
+        int lo = 0, hi = -1;
+        if (sl < na_) {
+            const float ac = fmaf((float)sl, da, a0);
+            const float pa = ac - ha - Sa, pb = ac + ha - Sa;
+            if (pa * sgn > 0.f && pb * sgn > 0.f) {
+                const float y1 = fmaf(pa, kl, So), y2 = fmaf(pb, kl, So);
+                const float y3 = fmaf(pa, kr, So), y4 = fmaf(pb, kr, So);
+                const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - o0) * inv_do + 0.5f;
+                const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - o0) * inv_do + 0.5f;
+                if (f1 >= -1.f && f0 <= (float)no_ + 1.f) {
+                    lo = max((int)floorf(f0 - 1e-3f), 0);
+                    hi = min((int)floorf(f1 + 1e-3f), no_ - 1);
+                }
             }
         }
-        acc[t * FWD_BS + tid] = fmaf(L, cur, acc[t * FWD_BS + tid]);
-    };
-
-    if (xstep) {
-        const float kl = dly / dlx, kr = dry / drx;
-        const float sgn = dlx > 0.f ? 1.f : -1.f;
-        for (int i = 0; i < G.nx; i++) {
-            const float xc = fmaf((float)i, G.dx, G.x0);
-            const float xa_ = xc - hx - Sx, xb_ = xc + hx - Sx;
-            if (xa_ * sgn <= 0.f || xb_ * sgn <= 0.f) continue;  // behind the source
-            const float y1 = fmaf(xa_, kl, Sy), y2 = fmaf(xb_, kl, Sy);
-            const float y3 = fmaf(xa_, kr, Sy), y4 = fmaf(xb_, kr, Sy);
-            const float ymin = fminf(fminf(y1, y2), fminf(y3, y4));
-            const float ymax = fmaxf(fmaxf(y1, y2), fmaxf(y3, y4));
-            const float fy0 = (ymin - G.y0) / G.dy + 0.5f, fy1 = (ymax - G.y0) / G.dy + 0.5f;
-            if (fy1 < -1.f || fy0 > (float)G.ny + 1.f) continue;
-            const int jlo = max((int)floorf(fy0) - 1, 0);
-            const int jhi = min((int)floorf(fy1) + 1, G.ny - 1);
-            for (int j = jlo; j <= jhi; j++) visit(i, j);
-        }
-    } else {
-        const float kl = dlx / dly, kr = drx / dry;
-        const float sgn = dly > 0.f ? 1.f : -1.f;
-        for (int j = 0; j < G.ny; j++) {
-            const float yc = fmaf((float)j, G.dy, G.y0);
-            const float ya_ = yc - hy - Sy, yb_ = yc + hy - Sy;
-            if (ya_ * sgn <= 0.f || yb_ * sgn <= 0.f) continue;
-            const float x1 = fmaf(ya_, kl, Sx), x2 = fmaf(yb_, kl, Sx);
-            const float x3 = fmaf(ya_, kr, Sx), x4 = fmaf(yb_, kr, Sx);
-            const float xmin = fminf(fminf(x1, x2), fminf(x3, x4));
-            const float xmax = fmaxf(fmaxf(x1, x2), fmaxf(x3, x4));
-            const float fx0 = (xmin - G.x0) / G.dx + 0.5f, fx1 = (xmax - G.x0) / G.dx + 0.5f;
-            if (fx1 < -1.f || fx0 > (float)G.nx + 1.f) continue;
-            const int ilo = max((int)floorf(fx0) - 1, 0);
-            const int ihi = min((int)floorf(fx1) + 1, G.nx - 1);
-            for (int i = ilo; i <= ihi; i++) visit(i, j);
+        const int npass = __reduce_max_sync(0xffffffffu, (hi - lo + F2_SUB) / F2_SUB);
+        for (int p = 0; p < npass; p++) {
+            const int o = lo + sub + F2_SUB * p;
+            if (o > hi) continue;
+            const int i = xstep ? sl : o, j = xstep ? o : sl;
+            const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
+            const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
+            if (fmaf(nlx, cx, nly * cy) + suppl < -tol_l || fmaf(nrx, cx, nry * cy) + suppr < -tol_r) continue;
+            Footprint f;
+            ct_footprint<ARC>(G, cb, sb, 0.f, i, j, f);
+            const float Lx = f.lxy * (ONES ? 1.f : __ldg(&x[(size_t)j * G.nx + i]));
+            float T0 = trap_T(f, ((float)s0 - 0.5f) - f.sfc);
+#pragma unroll
+            for (int c = 0; c < F2_CPW; c++) {
+                const float T1 = trap_T(f, ((float)(s0 + c) + 0.5f) - f.sfc);
+                acc[c] = fmaf(Lx, T1 - T0, acc[c]);
+                T0 = T1;
+            }
         }
     }
-
-    // epilogue: amplitude L_z, residual weighting (Eq. 36), write (coalesced over s)
-    for (int t = 0; t < nt; t++) {
-        const float q = (DIM == 3) ? acc[t * FWD_BS + tid] : q2d;
-        const float lz = (DIM == 3) ? ray_Lz<ARC>(G, s, t) : 1.f;
-        const size_t o = ((size_t)vi * nt + t) * G.ns + s;
-        const float p = lz * q;
+#pragma unroll
+    for (int c = 0; c < F2_CPW; c++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+    }
+    float q = acc[0];
+#pragma unroll
+    for (int c = 1; c < F2_CPW; c++) q = (lane == c) ? acc[c] : q;
+    const int s = s0 + lane;
+    if (lane < F2_CPW && s < G.ns) {
+        const size_t o = (size_t)vi * G.ns + s;
         if (MODE == FWD_PLAIN) {
-            out[o] = p;
+            out[o] = q;
         } else {
-            const size_t a = ((size_t)v * nt + t) * G.ns + s;
+            const size_t a = (size_t)v * G.ns + s;
             const float wv = w ? __ldg(&w[a]) : 1.f;
-            if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldg(&y[a]));
-            else out[o] = lz * wv * p;
+            if (MODE == FWD_RESID) out[o] = wv * (q - __ldg(&y[a]));
+            else out[o] = wv * q;
         }
     }
 }
-
 
 // ---------------------------------------------------------------------------
 // 3-D forward projection.  A warp owns F3_CPW = 4 adjacent detector columns
@@ -187,11 +155,12 @@ k_fwd(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vie
 // credited to the four detector columns with their own L = L_xy F1 (a voxel
 // column's footprint covers ~2.4 detector columns, so this removes most of the
 // redundant resampling of a one-column-per-warp walk).
-//   PFX (solve path): the x-update writes the z-prefix P_k = sum_{k'<k} x_k'
-//     of every voxel column (z-fastest, stride pfx_stride).  The magnified
-//     column is a piecewise-linear cumulative X(u) = H (P_k + frac x_k) over
-//     row units u, and the exact F2-weighted row sum is X(t+1) - X(t): RPL+1
-//     interpolations per lane, no per-voxel loop, no divergence.
+//   PFX (solve path): the x-update writes (P_k, x_k), P_k = sum_{k'<k} x_k',
+//     of every voxel column (float2, z-fastest, stride pfx_stride).  The
+//     magnified column is a piecewise-linear cumulative X(u) = H (P_k + frac x_k)
+//     over row units u, and the exact F2-weighted row sum is X(t+1) - X(t):
+//     RPL interpolations (one 8-byte gather each) per lane plus one shuffle,
+//     no per-voxel loop, no divergence.
 //   direct (ct_forward / init / D_L): row t loops over the voxels whose
 //     magnified extent [b_k, b_k+1] meets [t, t+1] (same overlap arithmetic as
 //     the back-projector), reading x in the boundary layout.
@@ -221,6 +190,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const int s0 = sb0 + wid * F3_CPW;             // first detector column of the warp
     const float* __restrict__ x = xa;
     if (ctl && !PFX) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
+    const float2* __restrict__ Q = reinterpret_cast<const float2*>(xa);  // PFX: z-prefix array
     const float4 vw = __ldg(&vtab[v]);
     const float cb = vw.x, sb = vw.y, zs = vw.z;
     const float Sx = G.dso * cb, Sy = G.dso * sb;
@@ -311,7 +281,15 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             eL = make_float4(Ls * Fc[0], Ls * Fc[1], Ls * Fc[2], Ls * Fc[3]);
                             if (PFX) {
                                 const float invH = __fdividef(1.f, f.H);
-                                eG = make_float4(-f.B0 * invH, invH, __int_as_float(j * G.nx + i), 0.f);
+                                const float b0 = -f.B0 * invH;
+                                // X at the top boundary RPL*32 of the lanes' rows (lane 31 needs it)
+                                const float2* __restrict__ Qc =
+                                    Q + (unsigned)(j * G.nx + i) * (unsigned)pfx_stride;
+                                float ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), 0.f), fnz);
+                                const float rt = __fadd_rn(__fadd_rn(ft, -0.5f), 12582912.0f);
+                                const float2 qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
+                                const float xtop = fmaf(ft - (rt - 12582912.0f), qt.y, qt.x);
+                                eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), xtop);
                             } else {
                                 eG = make_float4(f.B0, f.H, __int_as_float(j * G.nx + i), 0.f);
                             }
@@ -332,23 +310,25 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const int col = __float_as_int(q.z);
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
-                        // column base (32-bit element index); P has entries 0..nz+1 (P_nz+1 = P_nz)
-                        const unsigned cbase = (unsigned)col * (unsigned)pfx_stride;
+                        // X(u) = H (P_k + frac x_k) at the lane's RPL lower row boundaries; the
+                        // upper boundary of its last row is the next lane's first (shuffle),
+                        // lane 31 takes the producer's X(RPL*32).
+                        const float2* __restrict__ Qc = Q + (unsigned)col * (unsigned)pfx_stride;
                         float Xp[RPL + 1];
 #pragma unroll
-                        for (int r = 0; r <= RPL; r++) {
+                        for (int r = 0; r < RPL; r++) {
                             float f = fmaf((float)(RPL * lane + r), q.y, q.x);
                             f = fminf(fmaxf(f, 0.f), fnz);
                             // k = round-to-nearest(f - 1/2) via the 1.5*2^23 magic number, so
                             // k <= f <= k+1 (at an integer f either neighbouring segment gives the
-                            // same X: X is continuous).  f - 1/2 is exact for 0 <= f < 2^22.
+                            // same X: X is continuous; Q_nz = (P_nz, 0)).
                             const float rm = __fadd_rn(__fadd_rn(f, -0.5f), 12582912.0f);
                             const int k = __float_as_int(rm) - 0x4B400000;
-                            const float fk = rm - 12582912.0f;
-                            const float* __restrict__ pp = x + (cbase + (unsigned)k);
-                            const float p0 = __ldg(pp), p1 = __ldg(pp + 1);
-                            Xp[r] = fmaf(f - fk, p1 - p0, p0);
+                            const float2 qk = __ldg(Qc + k);
+                            Xp[r] = fmaf(f - (rm - 12582912.0f), qk.y, qk.x);
                         }
+                        const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);
+                        Xp[RPL] = lane == 31 ? q.w : xn;
 #pragma unroll
                         for (int r = 0; r < RPL; r++) Rs[r] = Xp[r + 1] - Xp[r];
                     } else {
@@ -437,26 +417,15 @@ static void fwd3_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Vi
     }
 }
 
-template <bool ARC, int DIM>
-static void fwd_dispatch_mode(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
-                              const float* xa, const float* xb, const float* y, const float* w, float* out,
-                              int mode, cudaStream_t s) {
-    dim3 grid((G.ns + FWD_BS - 1) / FWD_BS, max_count);
-    size_t smem = (DIM == 3) ? (size_t)G.nt * FWD_BS * sizeof(float) : 0;
-    switch (mode) {
-        case FWD_PLAIN:
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fwd<ARC, DIM, FWD_PLAIN><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-            break;
-        case FWD_RESID:
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fwd<ARC, DIM, FWD_RESID><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-            break;
-        default:
-            if (smem > 48 * 1024) cudaFuncSetAttribute(k_fwd<ARC, DIM, FWD_ONES_W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            k_fwd<ARC, DIM, FWD_ONES_W><<<grid, FWD_BS, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-            break;
-    }
+template <bool ARC>
+static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
+                          const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
+                          cudaStream_t s) {
+    dim3 grid((G.ns + F2_CPW * F2_WARPS - 1) / (F2_CPW * F2_WARPS), max_count);
+    const int bs = 32 * F2_WARPS;
+    if (mode == FWD_PLAIN) k_fwd2<ARC, FWD_PLAIN><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+    else if (mode == FWD_RESID) k_fwd2<ARC, FWD_RESID><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+    else k_fwd2<ARC, FWD_ONES_W><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
 }
 
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
@@ -465,10 +434,10 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
     if (max_count <= 0) return;
     if (G.arc) {
         if (G.dim == 3) fwd3_dispatch<true>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, pfx_stride, s);
-        else fwd_dispatch_mode<true, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        else fwd2_dispatch<true>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     } else {
         if (G.dim == 3) fwd3_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, pfx_stride, s);
-        else fwd_dispatch_mode<false, 2>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
+        else fwd2_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     }
     launches_add(1);
 }

@@ -12,6 +12,9 @@
 //   x+  = clamp(x - (s + grad)/(rho D_L + D_R), box)   (denominator 0 keeps x)
 //   htilde_partial = (1 - alpha) (D_L (x+ - x) + htilde)   (completed by the
 //                     back-projection epilogue: htilde+ = htilde_partial + alpha zeta)
+#include <algorithm>
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace ctr {
@@ -42,7 +45,7 @@ __device__ __forceinline__ void potential(float t, float inv_delta, float& dphi,
         om = 1.f;
     } else if (POT == 1) {   // hyperbola
         const float u = t * inv_delta;
-        om = rsqrtf(fmaf(u, u, 1.f));
+        om = rsqrt_ftz(fmaf(u, u, 1.f));
         dphi = t * om;
     } else {                 // Fair
         om = 1.f / fmaf(fabsf(t), inv_delta, 1.f);
@@ -93,12 +96,16 @@ __global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float*
     if (curv) curv[idx] = cv;
 }
 
-template <int NDIRS, bool KAPPA, int POT>
+// 26/8-neighbour sum over a register window W[slot][dy+1][dx+1] whose planes
+// z-1, z, z+1 sit in slots ZA, ZB, ZC (compile-time, so a z-march can rotate
+// the slots instead of moving registers).  CHECK = false is the interior path:
+// every neighbour exists, no predicates at all.
+template <int NDIRS, bool KAPPA, int POT, int ZA, int ZB, int ZC, bool CHECK>
 __device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const float (&K)[3][3][3],
                                                const RegParams& rp, bool im, bool ip, bool jm, bool jp, bool km,
                                                bool kp, float& grad, float& curv) {
-    const float xv = W[1][1][1];
-    const float kj = KAPPA ? K[1][1][1] : 1.f;
+    const float xv = W[ZB][1][1];
+    const float kj = KAPPA ? K[ZB][1][1] : 1.f;
     float gs = 0.f, cs = 0.f;
 #pragma unroll
     for (int d = 0; d < NDIRS; d++) {
@@ -107,12 +114,13 @@ __device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const 
             const int ox = sg ? -dir_x(d) : dir_x(d);
             const int oy = sg ? -dir_y(d) : dir_y(d);
             const int oz = sg ? -dir_z(d) : dir_z(d);
-            const bool ok = (ox < 0 ? im : (ox > 0 ? ip : true)) && (oy < 0 ? jm : (oy > 0 ? jp : true)) &&
-                            (oz < 0 ? km : (oz > 0 ? kp : true));
+            const int zs = oz < 0 ? ZA : (oz > 0 ? ZC : ZB);
+            const bool ok = !CHECK || ((ox < 0 ? im : (ox > 0 ? ip : true)) && (oy < 0 ? jm : (oy > 0 ? jp : true)) &&
+                                       (oz < 0 ? km : (oz > 0 ? kp : true)));
             if (ok) {
-                const float wgt = KAPPA ? rp.beta[d] * kj * K[1 + oz][1 + oy][1 + ox] : rp.beta[d];
+                const float wgt = KAPPA ? rp.beta[d] * kj * K[zs][1 + oy][1 + ox] : rp.beta[d];
                 float dphi, om;
-                potential<POT>(xv - W[1 + oz][1 + oy][1 + ox], rp.inv_delta, dphi, om);
+                potential<POT>(xv - W[zs][1 + oy][1 + ox], rp.inv_delta, dphi, om);
                 gs = fmaf(wgt, dphi, gs);
                 cs = fmaf(wgt, om, cs);
             }
@@ -122,88 +130,79 @@ __device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const 
     curv = 2.f * cs;
 }
 
-// Fused stencil + x-update, z-marching: thread = one voxel column (i, j), all
-// nz voxels; a warp = 32 consecutive i at one j.  The 3x3x3 neighbourhood of x
-// (and kappa) lives in registers and advances one plane per voxel (9 loads per
-// voxel instead of 27).  x+ and htilde_partial are written in the boundary
-// layout (coalesced over i).  With pfx != nullptr the thread also forms the
-// z-prefix P_k = sum_{k'<k} x+_k' of its column for the forward projector;
-// 32 prefix values per column are staged in shared memory and written as
-// whole 128-byte lines (z-fastest layout, column stride pfx_stride_of(G)).
+// Fused stencil + x-update.  Block = 32 consecutive i (a warp) x NZC z-chunks
+// x JPB rows j; thread = one voxel column (i, j) over the z-chunk
+// [c CZ, (c+1) CZ).  The 3x3x3 neighbourhood of x (and kappa) lives in
+// registers; the z-march rotates the three plane slots (unrolled by 3), so
+// each voxel costs 9 window loads and no register moves.  Interior columns
+// and planes take a predicate-free stencil (warp-uniform except in the edge
+// warps).  x+ and htilde_partial are written in the boundary layout
+// (coalesced over i).  With pfx != nullptr the block also forms the z-prefix
+// P_k = sum_{k'<k} x+_k' of its columns for the forward projector: x+ of the
+// column tile is kept in shared memory, chunk totals are scanned across the
+// NZC chunks, and each thread writes the prefix entries of its chunk
+// (float2 (P_k, x_k), z-fastest, column stride pfx_stride_of(G)).
 template <int POT, int NDIRS, bool KAPPA>
-__global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
+__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
                                                 float* xb, const float* __restrict__ dl,
                                                 const float* __restrict__ g, float* __restrict__ ht,
                                                 const float* __restrict__ kappa, float box_lo, float box_hi,
-                                                float* __restrict__ pfx) {
-    __shared__ float pst[4][32][33];
-    const int lane = threadIdx.x, wy = threadIdx.y;
+                                                float* __restrict__ pfx, int CZ) {
+    extern __shared__ float upd_sm[];  // pfx: xs[JPB][nz][33], tot[JPB][NZC][32]
+    const int lane = threadIdx.x, c = threadIdx.y, jj = threadIdx.z;
+    const int NZC = blockDim.y;
     const int i = blockIdx.x * 32 + lane;
-    const int j = blockIdx.y * 4 + wy;
+    const int j = blockIdx.y * blockDim.z + jj;
     const bool act = i < G.nx && j < G.ny;
-    if (j >= G.ny) return;  // warp-uniform (whole warp shares j)
     const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
     const float* __restrict__ x = odd ? xb : xa;
     float* __restrict__ xn = odd ? xa : xb;
     const float rho = rho_of_k(ctl);
     const float alpha = ctl->alpha;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
-    const size_t col = (size_t)j * G.nx + (act ? i : 0);
-    const int ps = pfx_stride_of(G);
+    const bool inxy = act && im && ip && jm && jp;
+    const size_t col = (size_t)(j < G.ny ? j : 0) * G.nx + (act ? i : 0);
+    const int k0 = c * CZ, k1 = min(G.nz, k0 + CZ);
+    float* xs = upd_sm + (size_t)jj * G.nz * 33;
+    float* tot = upd_sm + (size_t)blockDim.z * G.nz * 33 + (size_t)(jj * NZC) * 32;
     float W[3][3][3], K[3][3][3];
     auto load_plane = [&](int slot, int k) {
         const bool ok = act && k >= 0 && k < G.nz;
+        const float* __restrict__ xp = x + ((long long)k * G.nxy + (long long)col);
+        const float* __restrict__ kp_ = KAPPA ? kappa + ((long long)k * G.nxy + (long long)col) : nullptr;
+        if (inxy) {
 #pragma unroll
-        for (int dy = -1; dy <= 1; dy++) {
+            for (int dy = -1; dy <= 1; dy++)
 #pragma unroll
-            for (int dx = -1; dx <= 1; dx++) {
-                const bool v = ok && (dx < 0 ? im : (dx > 0 ? ip : true)) && (dy < 0 ? jm : (dy > 0 ? jp : true));
-                const size_t a = (size_t)k * G.nxy + col + (long long)dy * G.nx + dx;
-                W[slot][dy + 1][dx + 1] = v ? __ldg(&x[a]) : 0.f;
-                if (KAPPA) K[slot][dy + 1][dx + 1] = v ? __ldg(&kappa[a]) : 0.f;
-            }
-        }
-    };
-    auto flush = [&](int kb, int n) {  // prefix entries kb .. kb+n-1 of the warp's 32 columns
-        __syncwarp();
-        const int cbase = blockIdx.x * 32;
-        for (int c = 0; c < 32; c++) {
-            if (cbase + c < G.nx && lane < n)
-                pfx[((size_t)j * G.nx + cbase + c) * ps + kb + lane] = pst[wy][lane][c];
-        }
-        __syncwarp();
-    };
-    load_plane(1, -1);
-    load_plane(2, 0);
-    float run = 0.f;
-    int kb = 0, cnt = 0;
-    auto push = [&](float v) {
-        pst[wy][cnt][lane] = v;
-        if (++cnt == 32) {
-            flush(kb, 32);
-            kb += 32;
-            cnt = 0;
-        }
-    };
-    for (int k = 0; k < G.nz; k++) {
-#pragma unroll
-        for (int a = 0; a < 3; a++)
-#pragma unroll
-            for (int b = 0; b < 3; b++) {
-                W[0][a][b] = W[1][a][b];
-                W[1][a][b] = W[2][a][b];
-                if (KAPPA) {
-                    K[0][a][b] = K[1][a][b];
-                    K[1][a][b] = K[2][a][b];
+                for (int dx = -1; dx <= 1; dx++) {
+                    W[slot][dy + 1][dx + 1] = ok ? __ldg(xp + (dy * G.nx + dx)) : 0.f;
+                    if (KAPPA) K[slot][dy + 1][dx + 1] = ok ? __ldg(kp_ + (dy * G.nx + dx)) : 0.f;
                 }
-            }
-        load_plane(2, k + 1);
+        } else {
+#pragma unroll
+            for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+                for (int dx = -1; dx <= 1; dx++) {
+                    const bool v = ok && (dx < 0 ? im : (dx > 0 ? ip : true)) && (dy < 0 ? jm : (dy > 0 ? jp : true));
+                    W[slot][dy + 1][dx + 1] = v ? __ldg(xp + (dy * G.nx + dx)) : 0.f;
+                    if (KAPPA) K[slot][dy + 1][dx + 1] = v ? __ldg(kp_ + (dy * G.nx + dx)) : 0.f;
+                }
+        }
+    };
+    float run = 0.f;
+    // one voxel: planes k-1, k, k+1 in slots ZA, ZB, ZC; afterwards plane k+2 goes to ZA
+    auto step = [&](auto za, auto zb, auto zc, int k) {
+        constexpr int ZA = decltype(za)::value, ZB = decltype(zb)::value, ZC = decltype(zc)::value;
         float xnew = 0.f;
         if (act) {
             float gr, cv;
-            window_stencil<NDIRS, KAPPA, POT>(W, K, rp, im, ip, jm, jp, k > 0, k + 1 < G.nz, gr, cv);
+            const bool km = k > 0, kp = k + 1 < G.nz;
+            if (inxy && km && kp)
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gr, cv);
+            else
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gr, cv);
             const size_t idx = (size_t)k * G.nxy + col;
-            const float xv = W[1][1][1];
+            const float xv = W[ZB][1][1];
             const float d = __ldg(&dl[idx]);
             const float htv = ht[idx];
             const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
@@ -214,15 +213,37 @@ __global__ void __launch_bounds__(128) k_update(DGeom G, RegParams rp, const Ctl
             ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
         }
         if (pfx) {
-            push(run);   // P_k: prefix before voxel k
+            xs[k * 33 + lane] = xnew;
             run += xnew;
         }
+        load_plane(ZA, k + 2);
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    load_plane(0, k0 - 1);
+    load_plane(1, k0);
+    load_plane(2, k0 + 1);
+    for (int k = k0; k < k1; k += 3) {
+        step(I0(), I1(), I2(), k);
+        if (k + 1 >= k1) break;
+        step(I1(), I2(), I0(), k + 1);
+        if (k + 2 >= k1) break;
+        step(I2(), I0(), I1(), k + 2);
     }
-    if (pfx) {
-        push(run);  // P_nz
-        push(run);  // P_nz+1 = P_nz (padding read by the forward's interpolation)
-        if (cnt) flush(kb, cnt);
+    if (!pfx) return;
+    tot[c * 32 + lane] = run;
+    __syncthreads();
+    float P = 0.f;
+    for (int q = 0; q < c; q++) P += tot[q * 32 + lane];
+    if (!act) return;
+    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + col * (size_t)pfx_stride_of(G);
+    for (int k = k0; k < k1; k++) {
+        const float xk = xs[k * 33 + lane];
+        pc[k] = make_float2(P, xk);  // (P_k, x_k): prefix before voxel k and the voxel
+        P += xk;
     }
+    if (k1 == G.nz) pc[G.nz] = make_float2(P, 0.f);  // (P_nz, 0)
 }
 
 template <int POT, int NDIRS>
@@ -244,13 +265,38 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
     launches_add(1);
 }
 
+// launch shape of k_update: NZC z-chunks of CZ voxels, JPB rows per block (<= 256 threads)
+struct UpdShape {
+    int nzc, cz, jpb;
+    size_t smem;
+};
+static UpdShape upd_shape(const DGeom& G, bool pfx) {
+    UpdShape u;
+    u.nzc = std::min(8, std::max(1, G.nz / 12));
+    u.cz = (G.nz + u.nzc - 1) / u.nzc;
+    u.nzc = (G.nz + u.cz - 1) / u.cz;
+    u.jpb = std::max(1, 8 / u.nzc);
+    u.smem = pfx ? sizeof(float) * ((size_t)u.jpb * G.nz * 33 + (size_t)u.jpb * u.nzc * 32) : 0;
+    return u;
+}
+
+size_t update_smem_bytes(const DGeom& G) { return upd_shape(G, true).smem; }
+
 template <int POT, int NDIRS>
 static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                          const float* g, float* ht, const float* kappa, float lo, float hi, float* pfx,
                          cudaStream_t s) {
-    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4, 1);
-    if (kappa) k_update<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx);
-    else k_update<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx);
+    const UpdShape u = upd_shape(G, pfx != nullptr);
+    dim3 block(32, u.nzc, u.jpb), grid((G.nx + 31) / 32, (G.ny + u.jpb - 1) / u.jpb, 1);
+    if (kappa) {
+        if (u.smem > 48 * 1024)
+            cudaFuncSetAttribute(k_update<POT, NDIRS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)u.smem);
+        k_update<POT, NDIRS, true><<<grid, block, u.smem, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx, u.cz);
+    } else {
+        if (u.smem > 48 * 1024)
+            cudaFuncSetAttribute(k_update<POT, NDIRS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)u.smem);
+        k_update<POT, NDIRS, false><<<grid, block, u.smem, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx, u.cz);
+    }
 }
 
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
