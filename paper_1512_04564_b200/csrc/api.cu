@@ -106,7 +106,7 @@ static ct_status validate_desc(const ct_geom_desc* d) {
     if (!std::isfinite(d->orbit_deg) || !std::isfinite(d->orbit_start_deg) || !std::isfinite(d->pitch) ||
         !std::isfinite(d->source_z0))
         return fail(CT_E_CONFIG, "non-finite orbit parameters");
-    if ((long long)d->nx * d->ny * d->nz > (1LL << 33)) return fail(CT_E_CONFIG, "volume too large");
+    if ((long long)d->nx * d->ny * d->nz >= (1LL << 32)) return fail(CT_E_CONFIG, "volume of 2^32 voxels or more");
     if (d->nt > 128) return fail(CT_E_CONFIG, "nt = %d > 128 detector rows", d->nt);
     // the update kernel keeps x+ of a 32-column tile in shared memory for the z-prefix
     if (d->nz > 1536) return fail(CT_E_CONFIG, "nz = %d > 1536 slices", d->nz);

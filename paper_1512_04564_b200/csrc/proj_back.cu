@@ -71,6 +71,34 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     }
 }
 
+// Row sums of one (voxel column, view) over a window of W detector columns:
+// rs(t) = sum_q F[q] r[t][sw + q] (L_z(s, t) folded in when LZ), stored with
+// the running sum as cs[o] = (sum_{t' < t} rs, rs(t)).  The next row's W
+// gathers are issued before the current row's FMAs (software pipelining).
+template <bool ARC, bool LZ, int W>
+__device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[8], const float* __restrict__ pr,
+                                          int sw, int tw, int n, float2* __restrict__ cs, float& run) {
+    float a[W], b[W];
+#pragma unroll
+    for (int q = 0; q < W; q++) a[q] = __ldg(pr + q);
+    for (int o = 0; o < n; o++) {
+        const float* __restrict__ pn = pr + (o + 1 < n ? G.ns : 0);
+#pragma unroll
+        for (int q = 0; q < W; q++) b[q] = __ldg(pn + q);
+        float rs = 0.f;
+#pragma unroll
+        for (int q = 0; q < W; q++) {
+            const float wq = LZ ? F[q] * ray_Lz<ARC>(G, sw + q, tw + o) : F[q];
+            rs = fmaf(wq, a[q], rs);
+        }
+        cs[o * BK_BS] = make_float2(run, rs);
+        run += rs;
+        pr = pn;
+#pragma unroll
+        for (int q = 0; q < W; q++) a[q] = b[q];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // 3-D back-projection.  Thread = one voxel column (i, j) x a z-chunk of BK_KZ
 // voxels; block = 32 x BK_Y columns.  Per view:
@@ -126,16 +154,23 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         const int nc = shi - slo + 1;
         if (nc <= 0) continue;
         const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
-        // 4-column window [sw, sw + 3] inside the detector; F1 is exactly 0 outside [u0, u3]
-        const int sw = nc <= 4 ? max(min(slo, G.ns - 4), 0) : slo;
-        float F[4];
+        // warp-uniform window of W = 4 or 8 detector columns [sw, sw + W - 1] inside the
+        // detector (F1 is exactly 0 outside [u0, u3]); wider footprints take a general loop
+        const int ncmax = __reduce_max_sync(__activemask(), nc);
+        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= 8 && G.ns >= 8) ? 8 : 0;
+        const int sw = W ? max(min(slo, G.ns - W), 0) : slo;
+        float F[8];
         {
             float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
-                F[q] = (Tn - Tprev) * f.lxy;
-                Tprev = Tn;
+            for (int q = 0; q < 8; q++) {
+                if (q < 4 || W == 8) {
+                    const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
+                    F[q] = (Tn - Tprev) * f.lxy;
+                    Tprev = Tn;
+                } else {
+                    F[q] = 0.f;
+                }
             }
         }
         const float Bs = B0 - 0.5f;  // voxel boundary in row units minus (row + 1/2) below
@@ -143,27 +178,11 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
             const int twe = min(t1, tw + RM - 1);
             const int n = twe - tw + 1;
             float run = 0.f;
-            const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns);
-            if (nc <= 4 && G.ns >= 4) {
-                pr += sw;
-                for (int o = 0; o < n; o++) {
-                    float rs;
-                    if (LZ) {
-                        const int t = tw + o;
-                        rs = F[0] * ray_Lz<ARC>(G, sw, t) * __ldg(pr);
-                        rs = fmaf(F[1] * ray_Lz<ARC>(G, sw + 1, t), __ldg(pr + 1), rs);
-                        rs = fmaf(F[2] * ray_Lz<ARC>(G, sw + 2, t), __ldg(pr + 2), rs);
-                        rs = fmaf(F[3] * ray_Lz<ARC>(G, sw + 3, t), __ldg(pr + 3), rs);
-                    } else {
-                        rs = F[0] * __ldg(pr);
-                        rs = fmaf(F[1], __ldg(pr + 1), rs);
-                        rs = fmaf(F[2], __ldg(pr + 2), rs);
-                        rs = fmaf(F[3], __ldg(pr + 3), rs);
-                    }
-                    cs[o * BK_BS] = make_float2(run, rs);
-                    run += rs;
-                    pr += G.ns;
-                }
+            const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns + (unsigned)sw);
+            if (W == 4) {
+                back_rows<ARC, LZ, 4>(G, F, pr, sw, tw, n, cs, run);
+            } else if (W == 8) {
+                back_rows<ARC, LZ, 8>(G, F, pr, sw, tw, n, cs, run);
             } else {
                 // wide footprint (near the source in steep geometries): F1 on the fly
                 for (int o = 0; o < n; o++) {
@@ -173,7 +192,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                     for (int q = 0; q < nc; q++) {
                         const float Tn = trap_T(f, ((float)(slo + q) + 0.5f) - f.sfc);
                         const float wq = LZ ? (Tn - Tprev) * f.lxy * ray_Lz<ARC>(G, slo + q, t) : (Tn - Tprev) * f.lxy;
-                        rs = fmaf(wq, __ldg(pr + slo + q), rs);
+                        rs = fmaf(wq, __ldg(pr + q), rs);
                         Tprev = Tn;
                     }
                     cs[o * BK_BS] = make_float2(run, rs);

@@ -13,6 +13,7 @@
 //   htilde_partial = (1 - alpha) (D_L (x+ - x) + htilde)   (completed by the
 //                     back-projection epilogue: htilde+ = htilde_partial + alpha zeta)
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.cuh"
@@ -96,52 +97,76 @@ __global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float*
     if (curv) curv[idx] = cv;
 }
 
-// 26/8-neighbour sum over a register window W[slot][dy+1][dx+1] whose planes
-// z-1, z, z+1 sit in slots ZA, ZB, ZC (compile-time, so a z-march can rotate
-// the slots instead of moving registers).  CHECK = false is the interior path:
-// every neighbour exists, no predicates at all.
+// Potential in scaled form: tp = t / delta.  Returns omega(t) = phi'(t)/t and
+// tp * omega; phi'(t) = delta * tp * omega for all three potentials.
+template <int POT>
+__device__ __forceinline__ float omega_scaled(float tp) {
+    if (POT == 0) return 1.f;                                   // quadratic
+    if (POT == 1) return rsqrt_ftz(fmaf(tp, tp, 1.f));          // hyperbola
+    return __fdividef(1.f, 1.f + fabsf(tp));                    // Fair
+}
+
+// 26/8-neighbour sums over a register window W[slot][dy+1][dx+1] of x/delta
+// whose planes z-1, z, z+1 sit in ring slots ZA, ZB, ZC (compile-time, so the
+// z-march rotates slots instead of moving registers).  Returns
+// gs = sum_n w_n tp_n omega_n and cs = sum_n w_n omega_n (w_n = beta kappa_j
+// kappa_n); grad = delta gs, curv = 2 cs.  CHECK = false is the interior path:
+// every neighbour exists, no predicates, and without kappa the two
+// neighbours of a direction share one beta multiply.
 template <int NDIRS, bool KAPPA, int POT, int ZA, int ZB, int ZC, bool CHECK>
-__device__ __forceinline__ void window_stencil(const float (&W)[3][3][3], const float (&K)[3][3][3],
+__device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const float (&K)[4][3][3],
                                                const RegParams& rp, bool im, bool ip, bool jm, bool jp, bool km,
-                                               bool kp, float& grad, float& curv) {
+                                               bool kp, float& gs_out, float& cs_out) {
     const float xv = W[ZB][1][1];
     const float kj = KAPPA ? K[ZB][1][1] : 1.f;
     float gs = 0.f, cs = 0.f;
 #pragma unroll
     for (int d = 0; d < NDIRS; d++) {
+        const int ox = dir_x(d), oy = dir_y(d), oz = dir_z(d);
+        const int zp = oz > 0 ? ZC : ZB, zm = oz > 0 ? ZA : ZB;
+        if (!CHECK && !KAPPA) {
+            const float tp = xv - W[zp][1 + oy][1 + ox];
+            const float tm = xv - W[zm][1 - oy][1 - ox];
+            const float op = omega_scaled<POT>(tp), om = omega_scaled<POT>(tm);
+            gs = fmaf(rp.beta[d], fmaf(tp, op, tm * om), gs);
+            cs = fmaf(rp.beta[d], op + om, cs);
+        } else {
 #pragma unroll
-        for (int sg = 0; sg < 2; sg++) {
-            const int ox = sg ? -dir_x(d) : dir_x(d);
-            const int oy = sg ? -dir_y(d) : dir_y(d);
-            const int oz = sg ? -dir_z(d) : dir_z(d);
-            const int zs = oz < 0 ? ZA : (oz > 0 ? ZC : ZB);
-            const bool ok = !CHECK || ((ox < 0 ? im : (ox > 0 ? ip : true)) && (oy < 0 ? jm : (oy > 0 ? jp : true)) &&
-                                       (oz < 0 ? km : (oz > 0 ? kp : true)));
-            if (ok) {
-                const float wgt = KAPPA ? rp.beta[d] * kj * K[zs][1 + oy][1 + ox] : rp.beta[d];
-                float dphi, om;
-                potential<POT>(xv - W[zs][1 + oy][1 + ox], rp.inv_delta, dphi, om);
-                gs = fmaf(wgt, dphi, gs);
-                cs = fmaf(wgt, om, cs);
+            for (int sg = 0; sg < 2; sg++) {
+                const int sx = sg ? -ox : ox, sy = sg ? -oy : oy, sz = sg ? -oz : oz;
+                const int zs = sg ? zm : zp;
+                const bool ok = !CHECK || ((sx < 0 ? im : (sx > 0 ? ip : true)) &&
+                                           (sy < 0 ? jm : (sy > 0 ? jp : true)) &&
+                                           (sz < 0 ? km : (sz > 0 ? kp : true)));
+                if (ok) {
+                    const float wgt = KAPPA ? rp.beta[d] * kj * K[zs][1 + sy][1 + sx] : rp.beta[d];
+                    const float t = xv - W[zs][1 + sy][1 + sx];
+                    const float o = omega_scaled<POT>(t);
+                    gs = fmaf(wgt, t * o, gs);
+                    cs = fmaf(wgt, o, cs);
+                }
             }
         }
     }
-    grad = gs;
-    curv = 2.f * cs;
+    gs_out = gs;
+    cs_out = cs;
 }
 
-// Fused stencil + x-update.  Block = 32 consecutive i (a warp) x NZC z-chunks
-// x JPB rows j; thread = one voxel column (i, j) over the z-chunk
-// [c CZ, (c+1) CZ).  The 3x3x3 neighbourhood of x (and kappa) lives in
-// registers; the z-march rotates the three plane slots (unrolled by 3), so
-// each voxel costs 9 window loads and no register moves.  Interior columns
-// and planes take a predicate-free stencil (warp-uniform except in the edge
-// warps).  x+ and htilde_partial are written in the boundary layout
-// (coalesced over i).  With pfx != nullptr the block also forms the z-prefix
-// P_k = sum_{k'<k} x+_k' of its columns for the forward projector: x+ of the
-// column tile is kept in shared memory, chunk totals are scanned across the
-// NZC chunks, and each thread writes the prefix entries of its chunk
-// (float2 (P_k, x_k), z-fastest, column stride pfx_stride_of(G)).
+// Fused stencil + x-update (Algorithm 1 lines 4-5).  Block = 32 consecutive i
+// (a warp) x NZC z-chunks x JPB rows j; thread = one voxel column (i, j) over
+// the z-chunk [c CZ, (c+1) CZ).  The 3x3 neighbourhood of x/delta (and kappa)
+// of four planes lives in a register ring: plane k+2 and D_L, g, htilde of
+// voxel k+1 are fetched at the top of step k and first touched one step later
+// (a full stencil of latency hiding); the march is unrolled by 4 so the ring
+// slots are compile-time.
+// Interior columns and planes take the predicate-free stencil (warp-uniform
+// except in the edge warps); the JPB rows of a block share their x rows in L1.
+// x+ and htilde_partial are written in the boundary layout (coalesced over i).
+// With pfx != nullptr the block also forms the z-prefix of its columns for the
+// forward projector: x+ of the column tile is kept in shared memory, chunk
+// totals are scanned across the NZC chunks, and each thread writes the
+// entries of its chunk (float2 (P_k, x_k), z-fastest, column stride
+// pfx_stride_of(G)).  32-bit element offsets (nvox < 2^32, ct_geom_create).
 template <int POT, int NDIRS, bool KAPPA>
 __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
                                                 float* xb, const float* __restrict__ dl,
@@ -159,56 +184,74 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
     float* __restrict__ xn = odd ? xa : xb;
     const float rho = rho_of_k(ctl);
     const float alpha = ctl->alpha;
+    const float idel = rp.inv_delta, del = rp.delta;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
     const bool inxy = act && im && ip && jm && jp;
-    const size_t col = (size_t)(j < G.ny ? j : 0) * G.nx + (act ? i : 0);
+    const unsigned nx = (unsigned)G.nx, nxy = (unsigned)G.nxy;
+    const unsigned col = act ? (unsigned)j * nx + (unsigned)i : 0u;
     const int k0 = c * CZ, k1 = min(G.nz, k0 + CZ);
     float* xs = upd_sm + (size_t)jj * G.nz * 33;
     float* tot = upd_sm + (size_t)blockDim.z * G.nz * 33 + (size_t)(jj * NZC) * 32;
-    float W[3][3][3], K[3][3][3];
-    auto load_plane = [&](int slot, int k) {
+    float W[4][3][3], K[4][3][3], XC[4];
+    float Dv[2], Gv[2], Hv[2];  // D_L, g, htilde of the current / next voxel
+    // raw loads into a ring slot; the slot is scaled by 1/delta one step later
+    auto load_plane = [&](auto slot_c, int k) {
+        constexpr int S = decltype(slot_c)::value;
         const bool ok = act && k >= 0 && k < G.nz;
-        const float* __restrict__ xp = x + ((long long)k * G.nxy + (long long)col);
-        const float* __restrict__ kp_ = KAPPA ? kappa + ((long long)k * G.nxy + (long long)col) : nullptr;
-        if (inxy) {
+        const unsigned o = ok ? (unsigned)k * nxy + col : 0u;
 #pragma unroll
-            for (int dy = -1; dy <= 1; dy++)
+        for (int dy = -1; dy <= 1; dy++) {
+            const bool vy = inxy || (dy < 0 ? jm : (dy > 0 ? jp : true));
+            const unsigned ro = o + (unsigned)(dy * (int)nx);
 #pragma unroll
-                for (int dx = -1; dx <= 1; dx++) {
-                    W[slot][dy + 1][dx + 1] = ok ? __ldg(xp + (dy * G.nx + dx)) : 0.f;
-                    if (KAPPA) K[slot][dy + 1][dx + 1] = ok ? __ldg(kp_ + (dy * G.nx + dx)) : 0.f;
-                }
-        } else {
-#pragma unroll
-            for (int dy = -1; dy <= 1; dy++)
-#pragma unroll
-                for (int dx = -1; dx <= 1; dx++) {
-                    const bool v = ok && (dx < 0 ? im : (dx > 0 ? ip : true)) && (dy < 0 ? jm : (dy > 0 ? jp : true));
-                    W[slot][dy + 1][dx + 1] = v ? __ldg(xp + (dy * G.nx + dx)) : 0.f;
-                    if (KAPPA) K[slot][dy + 1][dx + 1] = v ? __ldg(kp_ + (dy * G.nx + dx)) : 0.f;
-                }
+            for (int dx = -1; dx <= 1; dx++) {
+                const bool v = ok && vy && (inxy || (dx < 0 ? im : (dx > 0 ? ip : true)));
+                W[S][dy + 1][dx + 1] = v ? __ldg(x + (ro + (unsigned)dx)) : 0.f;
+                if (KAPPA) K[S][dy + 1][dx + 1] = v ? __ldg(kappa + (ro + (unsigned)dx)) : 0.f;
+            }
         }
     };
+    auto scale_plane = [&](auto slot_c) {
+        constexpr int S = decltype(slot_c)::value;
+        XC[S] = W[S][1][1];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int b = 0; b < 3; b++) W[S][a][b] *= idel;
+    };
+    auto load_vox = [&](auto par_c, int k) {
+        constexpr int Q = decltype(par_c)::value;
+        const bool ok = act && k < k1;
+        const unsigned idx = ok ? (unsigned)k * nxy + col : 0u;
+        Dv[Q] = ok ? __ldg(dl + idx) : 0.f;
+        Gv[Q] = ok ? __ldg(g + idx) : 0.f;
+        Hv[Q] = ok ? ht[idx] : 0.f;
+    };
     float run = 0.f;
-    // one voxel: planes k-1, k, k+1 in slots ZA, ZB, ZC; afterwards plane k+2 goes to ZA
-    auto step = [&](auto za, auto zb, auto zc, int k) {
+    // voxel k: planes k-1, k, k+1 in slots ZA, ZB, ZC (ZC loaded raw one step
+    // ago: scaled now); plane k+2 is fetched into ZD and D_L, g, htilde of
+    // voxel k+1 into the other parity -- both are consumed one step later.
+    auto step = [&](auto za, auto zb, auto zc, auto zd, int k) {
         constexpr int ZA = decltype(za)::value, ZB = decltype(zb)::value, ZC = decltype(zc)::value;
+        constexpr int Q = ZB & 1;
+        scale_plane(zc);
+        load_plane(zd, k + 2);
+        load_vox(std::integral_constant<int, Q ^ 1>(), k + 1);
         float xnew = 0.f;
         if (act) {
-            float gr, cv;
+            const unsigned idx = (unsigned)k * nxy + col;
+            float gs, cs;
             const bool km = k > 0, kp = k + 1 < G.nz;
             if (inxy && km && kp)
-                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gr, cv);
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
             else
-                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gr, cv);
-            const size_t idx = (size_t)k * G.nxy + col;
-            const float xv = W[ZB][1][1];
-            const float d = __ldg(&dl[idx]);
-            const float htv = ht[idx];
-            const float s = fmaf(rho, htv, (1.f - rho) * __ldg(&g[idx]));
-            const float den = fmaf(rho, d, cv);
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
+            const float xv = XC[ZB];
+            const float d = Dv[Q], htv = Hv[Q];
+            const float s = fmaf(rho, htv, (1.f - rho) * Gv[Q]);
+            const float den = fmaf(rho, d, 2.f * cs);
             xnew = xv;
-            if (den > 0.f) xnew = fminf(fmaxf(xv - (s + gr) / den, box_lo), box_hi);
+            if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(fmaf(del, gs, s), den), box_lo), box_hi);
             xn[idx] = xnew;
             ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
         }
@@ -216,20 +259,25 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
             xs[k * 33 + lane] = xnew;
             run += xnew;
         }
-        load_plane(ZA, k + 2);
     };
     using I0 = std::integral_constant<int, 0>;
     using I1 = std::integral_constant<int, 1>;
     using I2 = std::integral_constant<int, 2>;
-    load_plane(0, k0 - 1);
-    load_plane(1, k0);
-    load_plane(2, k0 + 1);
-    for (int k = k0; k < k1; k += 3) {
-        step(I0(), I1(), I2(), k);
+    using I3 = std::integral_constant<int, 3>;
+    load_plane(I0(), k0 - 1);
+    load_plane(I1(), k0);
+    load_plane(I2(), k0 + 1);
+    load_vox(I1(), k0);
+    scale_plane(I0());
+    scale_plane(I1());
+    for (int k = k0; k < k1; k += 4) {
+        step(I0(), I1(), I2(), I3(), k);
         if (k + 1 >= k1) break;
-        step(I1(), I2(), I0(), k + 1);
+        step(I1(), I2(), I3(), I0(), k + 1);
         if (k + 2 >= k1) break;
-        step(I2(), I0(), I1(), k + 2);
+        step(I2(), I3(), I0(), I1(), k + 2);
+        if (k + 3 >= k1) break;
+        step(I3(), I0(), I1(), I2(), k + 3);
     }
     if (!pfx) return;
     tot[c * 32 + lane] = run;
@@ -237,7 +285,7 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
     float P = 0.f;
     for (int q = 0; q < c; q++) P += tot[q * 32 + lane];
     if (!act) return;
-    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + col * (size_t)pfx_stride_of(G);
+    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + (size_t)col * (size_t)pfx_stride_of(G);
     for (int k = k0; k < k1; k++) {
         const float xk = xs[k * 33 + lane];
         pc[k] = make_float2(P, xk);  // (P_k, x_k): prefix before voxel k and the voxel
@@ -270,12 +318,18 @@ struct UpdShape {
     int nzc, cz, jpb;
     size_t smem;
 };
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 static UpdShape upd_shape(const DGeom& G, bool pfx) {
     UpdShape u;
-    u.nzc = std::min(8, std::max(1, G.nz / 12));
+    static const int zdiv = env_int("CTR_UPD_ZDIV", 32);  // tuning knob: voxels per z-chunk target
+    u.nzc = std::min(8, std::max(1, G.nz / std::max(1, zdiv)));
     u.cz = (G.nz + u.nzc - 1) / u.nzc;
     u.nzc = (G.nz + u.cz - 1) / u.cz;
-    u.jpb = std::max(1, 8 / u.nzc);
+    u.jpb = std::max(1, 8 / u.nzc);  // JPB rows per block share x rows in L1
     u.smem = pfx ? sizeof(float) * ((size_t)u.jpb * G.nz * 33 + (size_t)u.jpb * u.nzc * 32) : 0;
     return u;
 }
@@ -286,6 +340,8 @@ template <int POT, int NDIRS>
 static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                          const float* g, float* ht, const float* kappa, float lo, float hi, float* pfx,
                          cudaStream_t s) {
+    static const int nopfx = env_int("CTR_UPD_NOPFX", 0);  // timing experiment only: skips the prefix
+    if (nopfx) pfx = nullptr;
     const UpdShape u = upd_shape(G, pfx != nullptr);
     dim3 block(32, u.nzc, u.jpb), grid((G.nx + 31) / 32, (G.ny + u.jpb - 1) / u.jpb, 1);
     if (kappa) {
