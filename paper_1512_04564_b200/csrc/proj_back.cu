@@ -21,8 +21,8 @@ namespace ctr {
 
 constexpr int BK_Y = 4;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ_DEFAULT = 16;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24)
-constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 (more rows => several passes)
+constexpr int BK_KZ_DEFAULT = 24;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24 | 32)
+constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 at KZ = 16 (more rows => several passes)
 
 // 2-D back-projection: thread = one pixel; per view one footprint and the
 // F1-weighted sum over the <= kMaxCells cells it covers.
@@ -114,11 +114,11 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[8], c
 //      piecewise-linear cumulative R(u) = cs_o + frac rs_o (one 8-byte shared
 //      load per voxel boundary, magic-number floor).
 template <bool ARC, int EPI, bool LZ, int BK_KZ>
-__global__ void __launch_bounds__(BK_BS, 7)
+__global__ void __launch_bounds__(BK_BS, BK_KZ <= 16 ? 7 : BK_KZ <= 24 ? 4 : 3)
 k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
-    constexpr int RM = BK_RMAX3;
+    constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : 44;
     __shared__ float2 csb[RM + 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;
@@ -154,17 +154,17 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         const int nc = shi - slo + 1;
         if (nc <= 0) continue;
         const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
-        // warp-uniform window of W = 4 or 8 detector columns [sw, sw + W - 1] inside the
+        // warp-uniform window of W = 4, 6 or 8 detector columns [sw, sw + W - 1] inside the
         // detector (F1 is exactly 0 outside [u0, u3]); wider footprints take a general loop
         const int ncmax = __reduce_max_sync(__activemask(), nc);
-        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= 8 && G.ns >= 8) ? 8 : 0;
+        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= 6 && G.ns >= 6) ? 6 : (ncmax <= 8 && G.ns >= 8) ? 8 : 0;
         const int sw = W ? max(min(slo, G.ns - W), 0) : slo;
         float F[8];
         {
             float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
-                if (q < 4 || W == 8) {
+                if (q < 4 || q < W) {
                     const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
                     F[q] = (Tn - Tprev) * f.lxy;
                     Tprev = Tn;
@@ -181,6 +181,8 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
             const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns + (unsigned)sw);
             if (W == 4) {
                 back_rows<ARC, LZ, 4>(G, F, pr, sw, tw, n, cs, run);
+            } else if (W == 6) {
+                back_rows<ARC, LZ, 6>(G, F, pr, sw, tw, n, cs, run);
             } else if (W == 8) {
                 back_rows<ARC, LZ, 8>(G, F, pr, sw, tw, n, cs, run);
             } else {
@@ -292,7 +294,7 @@ static int back_kz() {
     static int kz = [] {
         const char* e = getenv("CTR_BK_KZ");
         const int v = e ? atoi(e) : BK_KZ_DEFAULT;
-        return (v == 8 || v == 24) ? v : 16;
+        return (v == 8 || v == 16 || v == 24 || v == 32) ? v : BK_KZ_DEFAULT;
     }();
     return kz;
 }
@@ -303,8 +305,9 @@ static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Vi
     if (DIM != 3) return back2_dispatch<ARC>(G, vtab, ctl, v, proj, scale, epi, out, g, ht, s);
     switch (back_kz()) {
         case 8: back3_dispatch_kz<ARC, 8>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        case 24: back3_dispatch_kz<ARC, 24>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
-        default: back3_dispatch_kz<ARC, 16>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 16: back3_dispatch_kz<ARC, 16>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        case 32: back3_dispatch_kz<ARC, 32>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
+        default: back3_dispatch_kz<ARC, 24>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s); break;
     }
 }
 
