@@ -82,6 +82,20 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return r;
 }
 
+// L2 evict-last policy for data re-read by many views (the forward's z-prefix
+// array) and a gather that carries it; streaming (evict-first) for data read
+// or written once per sub-iteration goes through __ldcs / __stcs.
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float ldg_keep(const float* p, unsigned long long pol) {
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ void sort4(float& a, float& b, float& c, float& d) {
     float t;
 #define CTR_CS(p, q) if (p > q) { t = p; p = q; q = t; }

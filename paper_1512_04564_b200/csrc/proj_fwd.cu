@@ -172,8 +172,11 @@ constexpr int F3_CPW = 4;
 constexpr int F3_BS = 32 * F3_WARPS;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
+#ifndef F3_MINB
+#define F3_MINB 4  // 64 registers: 4 blocks (32 warps) per SM to hide the prefix-gather latency
+#endif
 template <bool ARC, int MODE, int RPL, bool PFX>
-__global__ void __launch_bounds__(F3_BS)
+__global__ void __launch_bounds__(F3_BS, F3_MINB)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
@@ -384,9 +387,10 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         if (MODE == FWD_PLAIN) {
             out[o] = p;
         } else {
+            // y, w are read once per sub-iteration: streaming (evict-first) loads
             const size_t a = ((size_t)v * G.nt + t) * G.ns + ss;
-            const float wv = w ? __ldg(&w[a]) : 1.f;
-            if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldg(&y[a]));
+            const float wv = w ? __ldcs(&w[a]) : 1.f;
+            if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldcs(&y[a]));
             else out[o] = lz * wv * p;
         }
     }
