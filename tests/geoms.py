@@ -20,6 +20,17 @@ def tiny(kind, **over):
                   ds=1.5, dt=1.6, offset_s=1.25, offset_t=-0.2, dso=100.0, dsd=180.0, na=40,
                   orbit_deg=720.0, pitch=1.0)
         g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 1.0, 720.0)
+    elif kind == "helical_fine":
+        # fine detector pitch: voxel footprints span 3..11 columns, so the GPU back-projector's
+        # 4-, 6- and 8-column windows and its general (> 8 columns) loop all run
+        g = _geom(dim=3, nx=12, ny=12, nz=9, dx=1.0, dy=1.0, dz=0.8, det="arc", ns=104, nt=10,
+                  ds=0.3, dt=1.3, offset_s=0.75, offset_t=0.1, dso=100.0, dsd=180.0, na=30,
+                  orbit_deg=720.0, pitch=0.8)
+        g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 0.8, 720.0)
+    elif kind == "axial_fine":
+        g = _geom(dim=3, nx=10, ny=12, nz=6, dx=1.0, dy=0.9, dz=1.1, det="flat", ns=76, nt=12,
+                  ds=0.45, dt=1.7, offset_s=-0.4, offset_t=0.2, dso=100.0, dsd=180.0, na=16,
+                  orbit_start_deg=11.0)
     else:
         raise KeyError(kind)
     g.update(over)
@@ -27,3 +38,4 @@ def tiny(kind, **over):
 
 
 KINDS = ["fan2d_arc", "fan2d_flat", "axial_flat", "helical_arc"]
+FINE_KINDS = ["helical_fine", "axial_fine"]  # GPU parity only (wide-footprint code paths)

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 from oracle import alg  # noqa: E402
 from oracle import projector as P  # noqa: E402
-from tests.geoms import KINDS, tiny  # noqa: E402
+from tests.geoms import FINE_KINDS, KINDS, tiny  # noqa: E402
 from tests.problems import config_problem, oracle_problem, rel, synthetic_problem  # noqa: E402
 
 
@@ -37,7 +37,7 @@ def host(t):
     return t.double().cpu().numpy()
 
 
-GEOMS = {k: tiny(k) for k in KINDS}
+GEOMS = {k: tiny(k) for k in KINDS + FINE_KINDS}
 GEOMS["c1"] = None  # filled lazily from synth
 
 
@@ -48,7 +48,7 @@ def geom_of(name):
     return GEOMS[name]
 
 
-@pytest.mark.parametrize("name", KINDS + ["c1"])
+@pytest.mark.parametrize("name", KINDS + FINE_KINDS + ["c1"])
 def test_forward_back_parity(C, name):
     g = geom_of(name)
     rng = np.random.default_rng(7)
@@ -84,7 +84,7 @@ def test_forward_back_parity(C, name):
         C.ct_geom_destroy(h)
 
 
-@pytest.mark.parametrize("name", KINDS)
+@pytest.mark.parametrize("name", KINDS + FINE_KINDS)
 def test_sqs_diag_parity(C, name):
     g = geom_of(name)
     rng = np.random.default_rng(8)
@@ -133,7 +133,7 @@ def _gpu_recon(pb, dl=None):
     return r
 
 
-@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("kind", KINDS + FINE_KINDS)
 def test_solve_trace_matches_oracle(C, kind):
     """Per-step trace: x, g and htilde after sub-iterations 1, 2, 3, M, 2M."""
     pb = synthetic_problem(tiny(kind), M=3)
