@@ -183,7 +183,12 @@ ct_status oslalm_workspace_size(const ct_geom* g, const oslalm_params* p, const 
  * x_ref / rms_per_iter (host double[], one entry per completed outer
  * iteration within this call) are optional; giving them synchronises.
  * dist != NULL shards each subset's views over the ranks and sums the partial
- * back-projections with ncclAllReduce (all ranks hold the full volume).
+ * back-projections with ncclAllReduce (all ranks hold the full volume; P:470).
+ * While the all-reduce of sub-iteration j is in flight, grad R and D_R of the
+ * new x run on the communicator's side stream; sub-iteration j+1 then folds
+ * zeta into g, htilde (lines 7-8) and updates x (lines 4-5) in one kernel.
+ * The last zeta of a call is folded before the call returns, so a state
+ * handed back is always complete (resumable on any rank count).
  * Single-GPU calls replay a cached CUDA graph of one sub-iteration.
  * Errors: CT_E_CONFIG (alpha not in [1,2), rho_fixed <= 0, M < 1 or M > na,
  * box_lo > box_hi, bad regulariser), CT_E_NOMEM (workspace), CT_E_NUMERIC
@@ -221,7 +226,12 @@ double oslalm_rho(int64_t k, double alpha);
 ct_status ct_sync(ct_stream s);
 
 /* NCCL plumbing (one process per GPU).  The unique id (128 bytes) is created
- * on rank 0 and broadcast by the caller (e.g. torch.distributed). */
+ * on rank 0 and broadcast by the caller (e.g. torch.distributed).
+ * ct_dist_create makes the communicator of rank `rank` of `world` on CUDA
+ * device `device` (collective: every rank must call it), plus a
+ * high-priority side stream and two events owned by the handle (the
+ * stencil/all-reduce overlap of oslalm_relaxed_solve).  Errors: CT_E_CONFIG
+ * (rank/world), CT_E_NCCL, CT_E_CUDA.  ct_dist_destroy frees all of it. */
 ct_status ct_nccl_unique_id(unsigned char id[128]);
 ct_status ct_dist_create(int rank, int world, const unsigned char id[128], int device, ct_dist** out);
 void ct_dist_destroy(ct_dist* d);

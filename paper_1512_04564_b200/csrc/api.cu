@@ -71,6 +71,8 @@ struct ct_geom {
 struct ct_dist {
     ncclComm_t comm;
     int rank, world, device;
+    cudaStream_t side;              // high-priority stream: stencil of the new x during the all-reduce
+    cudaEvent_t ev_x, ev_sten;      // x+ written / stencil done
 };
 
 struct DeviceGuard {
@@ -299,7 +301,7 @@ extern "C" ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const f
 
 // ------------------------------------------------------------------ solver
 struct WsLayout {
-    size_t ctl, xalt, xt, r, zeta, flag, dsum, total;
+    size_t ctl, xalt, xt, r, zeta, gradr, curvr, flag, dsum, total;
 };
 
 static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -319,6 +321,10 @@ static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dis
     L.r = off;
     off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
     L.zeta = off;
+    if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
+    L.gradr = off;  // multi-GPU: grad R and D_R of the new x, computed during the all-reduce
+    if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
+    L.curvr = off;
     if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
     L.flag = off;
     off = align_up(off + sizeof(int));
@@ -395,6 +401,8 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     float* xt = g->G.dim == 3 ? (float*)(ws + L.xt) : nullptr;
     float* rbuf = (float*)(ws + L.r);
     float* zeta = dist ? (float*)(ws + L.zeta) : nullptr;
+    float* gradr = dist ? (float*)(ws + L.gradr) : nullptr;
+    float* curvr = dist ? (float*)(ws + L.curvr) : nullptr;
     int* dflag = (int*)(ws + L.flag);
     double* dsum = (double*)(ws + L.dsum);
     const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
@@ -489,12 +497,13 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         evs.resize((size_t)n_subiters * 5);
         for (auto& e : evs) CT_CUDA(cudaEventCreate(&e));
     }
+    bool pending = false;  // multi-GPU: zeta of the previous sub-iteration not yet folded into g, htilde
     while (done < n_subiters) {
         cudaEvent_t* ev = kernel_ms ? &evs[(size_t)done * 5] : nullptr;
         if (exec) {
             CT_CUDA(cudaGraphLaunch(exec, s));
             launches_add(4);
-        } else {
+        } else if (!dist) {
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
@@ -502,17 +511,43 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                                pfx_stride_of(g->G));
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
-            if (!dist) {
-                launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g,
-                            st->htilde, s);
-                if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
-            } else {
-                launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
-                if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
-                CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
-                launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
-            }
+            launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g, st->htilde, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
             launch_advance(ctl, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
+        } else {
+            // Multi-GPU sub-iteration.  The stencil of the new x runs on the
+            // side stream while this rank's projections and the zeta all-reduce proceed; the
+            // next sub-iteration folds zeta into g, htilde and updates x in one pass.
+            float* xin = (done & 1) ? xalt : st->x;
+            float* xout = (done & 1) ? st->x : xalt;
+            if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
+            if (!pending) {
+                launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
+            } else {
+                CT_CUDA(cudaStreamWaitEvent(s, dist->ev_sten, 0));
+                launch_update_pre(g->G, ctl, xin, xout, d_l, st->g, st->htilde, zeta, gradr, curvr, lo, hi, xt, s);
+                launch_advance(ctl, s);
+            }
+            if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
+            CT_CUDA(cudaEventRecord(dist->ev_x, s));
+            CT_CUDA(cudaStreamWaitEvent(dist->side, dist->ev_x, 0));
+            launch_reg(g->G, rp, xout, kappa, gradr, curvr, dist->side);
+            CT_CUDA(cudaEventRecord(dist->ev_sten, dist->side));
+            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s,
+                               pfx_stride_of(g->G));
+            else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
+            launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
+            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+            pending = true;
+            if (done + 1 == n_subiters) {
+                // fold the last zeta (lines 7-8) and advance: the state is complete on return
+                launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
+                launch_advance(ctl, s);
+                pending = false;
+            }
             if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
         }
         done++;
@@ -612,13 +647,26 @@ extern "C" ct_status ct_dist_create(int rank, int world, const unsigned char id[
     memcpy(u.internal, id, 128);
     ncclComm_t comm;
     CT_NCCL(ncclCommInitRank(&comm, world, u, rank));
-    ct_dist* d = new ct_dist{comm, rank, world, device};
+    ct_dist* d = new ct_dist{comm, rank, world, device, nullptr, nullptr, nullptr};
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&d->side, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_x, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_sten, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        ct_dist_destroy(d);
+        return fail(CT_E_CUDA, "ct_dist_create: %s", cudaGetErrorString(e));
+    }
     *out = d;
     return CT_OK;
 }
 
 extern "C" void ct_dist_destroy(ct_dist* d) {
     if (!d) return;
+    DeviceGuard guard(d->device);
+    if (d->ev_sten) cudaEventDestroy(d->ev_sten);
+    if (d->ev_x) cudaEventDestroy(d->ev_x);
+    if (d->side) cudaStreamDestroy(d->side);
     ncclCommDestroy(d->comm);
     delete d;
 }

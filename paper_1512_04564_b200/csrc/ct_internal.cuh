@@ -50,14 +50,15 @@ struct Views {          // explicit descriptor, or subset-from-Ctl when ctl != n
     int start, stride, count;
 };
 
-__device__ __forceinline__ float rho_of_k(const Ctl* c) {
+__device__ __forceinline__ float rho_at(const Ctl* c, long long k) {
     if (c->rho_fixed_mode) return c->rho_fixed;
-    long long k = c->k;
     if (k == 0) return 1.0f;
     double a = 3.14159265358979323846 / ((double)c->alpha * (double)(k + 1));
     double b = 0.5 * a;
     return (float)(a * sqrt(1.0 - b * b));
 }
+
+__device__ __forceinline__ float rho_of_k(const Ctl* c) { return rho_at(c, c->k); }
 
 // View selection: subset m = k mod M, sharded over ranks (rank p takes the
 // subset-local views p, p+G, ...).

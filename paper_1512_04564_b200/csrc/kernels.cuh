@@ -36,6 +36,13 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
                    const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s);
 
+// multi-GPU path: fold the all-reduced zeta of the previous sub-iteration into
+// g, htilde (lines 7-8) and run lines 4-5 from precomputed grad R / D_R
+// (launch_reg on the new x); Ctl.k is one behind (the advance follows)
+void launch_update_pre(const DGeom& G, const Ctl* ctl, const float* xin, float* xout, const float* dl, float* g,
+                       float* ht, const float* zeta, const float* grad, const float* curv, float box_lo,
+                       float box_hi, float* pfx, cudaStream_t s);
+
 // dist path: g, htilde update from an all-reduced zeta (lines 7-8)
 void launch_gh_update(const DGeom& G, const Ctl* ctl, const float* zeta, float* g, float* ht, cudaStream_t s);
 void launch_init_from_zeta(const DGeom& G, const float* zeta, float* g, float* ht, cudaStream_t s);

@@ -1,7 +1,8 @@
 // reg_update.cu — K4 regulariser stencil (Eq. 35) and the
-// fused Algorithm 1 x-update (lines 4-5), plus the small
-// elementwise kernels of the solver (dist-path g/htilde update, advance of
-// the Eq. 37 counter, htilde -> h, finiteness / RMS check).
+// fused Algorithm 1 x-update (lines 4-5), the multi-GPU
+// fold-and-update kernel, plus the small elementwise kernels of the solver
+// (dist-path g/htilde update, advance of the Eq. 37 counter, htilde -> h,
+// finiteness / RMS check).
 //
 // grad_j = sum_n beta_{d(j,n)} kappa_j kappa_n phi'(x_j - x_n)
 // D_R,j  = 2 sum_n beta_{d(j,n)} kappa_j kappa_n omega(x_j - x_n),  omega = phi'(t)/t
@@ -32,70 +33,6 @@ __host__ __device__ constexpr int dir_z(int d) { return d >= 4 ? 1 : 0; }
 static_assert(dir_x(6) == -1 && dir_y(8) == -1 && dir_z(4) == 1 && dir_x(4) == 0 && dir_y(12) == -1 &&
                   dir_x(11) == 1 && dir_y(11) == -1 && dir_z(3) == 0,
               "direction table");
-
-__constant__ int c_dirs[13][3] = {
-    {1, 0, 0}, {0, 1, 0}, {1, 1, 0}, {1, -1, 0},
-    {0, 0, 1}, {1, 0, 1}, {-1, 0, 1}, {0, 1, 1}, {0, -1, 1},
-    {1, 1, 1}, {-1, 1, 1}, {1, -1, 1}, {-1, -1, 1},
-};
-
-template <int POT>
-__device__ __forceinline__ void potential(float t, float inv_delta, float& dphi, float& om) {
-    if (POT == 0) {          // quadratic
-        dphi = t;
-        om = 1.f;
-    } else if (POT == 1) {   // hyperbola
-        const float u = t * inv_delta;
-        om = rsqrt_ftz(fmaf(u, u, 1.f));
-        dphi = t * om;
-    } else {                 // Fair
-        om = 1.f / fmaf(fabsf(t), inv_delta, 1.f);
-        dphi = t * om;
-    }
-}
-
-template <int POT, int NDIRS, bool KAPPA>
-__device__ __forceinline__ void stencil(const DGeom& G, const RegParams& rp, const float* __restrict__ x,
-                                        const float* __restrict__ kappa, int i, int j, int k, size_t idx,
-                                        float xv, float& grad, float& curv) {
-    const float kj = KAPPA ? __ldg(&kappa[idx]) : 1.f;
-    float gs = 0.f, cs = 0.f;
-#pragma unroll
-    for (int d = 0; d < NDIRS; d++) {
-        const int ox = c_dirs[d][0], oy = c_dirs[d][1], oz = c_dirs[d][2];
-        const long long off = (long long)oz * G.nxy + (long long)oy * G.nx + ox;
-        const float b = rp.beta[d];
-#pragma unroll
-        for (int sgn = 0; sgn < 2; sgn++) {
-            const int si = sgn ? -1 : 1;
-            const int ni = i + si * ox, nj = j + si * oy, nk = k + si * oz;
-            if (ni < 0 || nj < 0 || nk < 0 || ni >= G.nx || nj >= G.ny || nk >= G.nz) continue;
-            const size_t nb = (size_t)((long long)idx + si * off);
-            const float wgt = KAPPA ? b * kj * __ldg(&kappa[nb]) : b;
-            float dphi, om;
-            potential<POT>(xv - __ldg(&x[nb]), rp.inv_delta, dphi, om);
-            gs = fmaf(wgt, dphi, gs);
-            cs = fmaf(wgt, om, cs);
-        }
-    }
-    grad = gs;
-    curv = 2.f * cs;
-}
-
-template <int POT, int NDIRS, bool KAPPA>
-__global__ void __launch_bounds__(256) k_reg(DGeom G, RegParams rp, const float* __restrict__ x,
-                                             const float* __restrict__ kappa, float* __restrict__ grad,
-                                             float* __restrict__ curv) {
-    const int i = blockIdx.x * 32 + threadIdx.x;
-    const int j = blockIdx.y * 8 + threadIdx.y;
-    const int k = blockIdx.z;
-    if (i >= G.nx || j >= G.ny) return;
-    const size_t idx = (size_t)k * G.nxy + (size_t)j * G.nx + i;
-    float gr, cv;
-    stencil<POT, NDIRS, KAPPA>(G, rp, x, kappa, i, j, k, idx, __ldg(&x[idx]), gr, cv);
-    grad[idx] = gr;
-    if (curv) curv[idx] = cv;
-}
 
 // Potential in scaled form: tp = t / delta.  Returns omega(t) = phi'(t)/t and
 // tp * omega; phi'(t) = delta * tp * omega for all three potentials.
@@ -152,46 +89,88 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
     cs_out = cs;
 }
 
-// Fused stencil + x-update (Algorithm 1 lines 4-5).  Block = 32 consecutive i
-// (a warp) x NZC z-chunks x JPB rows j; thread = one voxel column (i, j) over
-// the z-chunk [c CZ, (c+1) CZ).  The 3x3 neighbourhood of x/delta (and kappa)
-// of four planes lives in a register ring: plane k+2 and D_L, g, htilde of
-// voxel k+1 are fetched at the top of step k and first touched one step later
-// (a full stencil of latency hiding); the march is unrolled by 4 so the ring
-// slots are compile-time.
-// Interior columns and planes take the predicate-free stencil (warp-uniform
-// except in the edge warps); the JPB rows of a block share their x rows in L1.
-// x+ and htilde_partial are written in the boundary layout (coalesced over i).
-// With pfx != nullptr the block also forms the z-prefix of its columns for the
-// forward projector: x+ of the column tile is kept in shared memory, chunk
-// totals are scanned across the NZC chunks, and each thread writes the
-// entries of its chunk (float2 (P_k, x_k), z-fastest, column stride
-// pfx_stride_of(G)).  32-bit element offsets (nvox < 2^32, ct_geom_create).
-template <int POT, int NDIRS, bool KAPPA>
-__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, float* xa,
-                                                float* xb, const float* __restrict__ dl,
-                                                const float* __restrict__ g, float* __restrict__ ht,
-                                                const float* __restrict__ kappa, float box_lo, float box_hi,
-                                                float* __restrict__ pfx, int CZ) {
+// Arguments of the update-family kernels (k_update, k_update_pre).
+struct UpdArgs {
+    float* xa;            // solver x double buffer (parity from Ctl unless xin is set)
+    float* xb;
+    const float* xin;     // UPD_STEN: explicit input image
+    const float* dl;      // D_L
+    float* g;             // g (k_update_pre folds the pending zeta into it)
+    float* ht;            // htilde
+    const float* kappa;   // NULL = ones
+    const float* zeta;    // k_update_pre: all-reduced zeta of the previous sub-iteration
+    const float* grad;    // k_update_pre: grad R(x) from the stencil kernel
+    const float* curv;    // k_update_pre: D_R(x)
+    float* grad_out;      // UPD_STEN outputs
+    float* curv_out;
+    float* pfx;           // z-prefix of x+ for the 3-D forward (NULL = none)
+    float box_lo, box_hi;
+    int CZ;               // voxels per z-chunk
+};
+
+enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
+
+// z-prefix of the block's x+ columns (x+ staged in shared memory xs[k][lane]):
+// chunk totals are scanned across the NZC chunks and each thread writes the
+// entries of its chunk, (P_k, x_k) as float2 (z-fastest, column stride
+// pfx_stride_of(G)), plus (P_nz, 0) from the last chunk.
+__device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__ pfx, const float* xs, float* tot,
+                                             float run, int c, int lane, bool act, unsigned col, int k0, int k1) {
+    tot[c * 32 + lane] = run;
+    __syncthreads();
+    float P = 0.f;
+    for (int q = 0; q < c; q++) P += tot[q * 32 + lane];
+    if (!act) return;
+    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + (size_t)col * (size_t)pfx_stride_of(G);
+    for (int k = k0; k < k1; k++) {
+        const float xk = xs[k * 33 + lane];
+        pc[k] = make_float2(P, xk);  // (P_k, x_k): prefix before voxel k and the voxel
+        P += xk;
+    }
+    if (k1 == G.nz) pc[G.nz] = make_float2(P, 0.f);  // (P_nz, 0)
+}
+
+// Stencil (+ x-update).  Block = 32 consecutive i (a warp) x NZC z-chunks x
+// JPB rows j; thread = one voxel column (i, j) over the z-chunk
+// [c CZ, (c+1) CZ).  The 3x3 neighbourhood of x/delta (and kappa) of four
+// planes lives in a register ring: plane k+2 and D_L, g, htilde of voxel k+1
+// are fetched at the top of step k and first touched one step later (a full
+// stencil of latency hiding); the march is unrolled by 4 so the ring slots are
+// compile-time.  Interior columns and planes take the predicate-free stencil
+// (warp-uniform except in the edge warps); the JPB rows of a block share their
+// x rows in L1.  32-bit element offsets (nvox < 2^32, ct_geom_create).
+//   UPD_FULL (Algorithm 1 lines 4-5, the solve path): x+ and htilde_partial in
+//     the boundary layout (coalesced over i); with pfx the z-prefix of x+.
+//   UPD_STEN (ct_reg_grad, and the multi-GPU path where the stencil of the new
+//     x overlaps the zeta all-reduce): grad R(x) and D_R(x) only.
+template <int POT, int NDIRS, bool KAPPA, int MODE>
+__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, UpdArgs A) {
     extern __shared__ float upd_sm[];  // pfx: xs[JPB][nz][33], tot[JPB][NZC][32]
+    constexpr bool FULL = (MODE == UPD_FULL);
     const int lane = threadIdx.x, c = threadIdx.y, jj = threadIdx.z;
     const int NZC = blockDim.y;
     const int i = blockIdx.x * 32 + lane;
     const int j = blockIdx.y * blockDim.z + jj;
     const bool act = i < G.nx && j < G.ny;
-    const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
-    const float* __restrict__ x = odd ? xb : xa;
-    float* __restrict__ xn = odd ? xa : xb;
-    const float rho = rho_of_k(ctl);
-    const float alpha = ctl->alpha;
+    const float* __restrict__ x = A.xin;
+    float* __restrict__ xn = nullptr;
+    float rho = 0.f, alpha = 0.f;
+    if (FULL) {
+        const bool odd = ((ctl->k - ctl->k_base) & 1) != 0;
+        x = odd ? A.xb : A.xa;
+        xn = odd ? A.xa : A.xb;
+        rho = rho_of_k(ctl);
+        alpha = ctl->alpha;
+    }
     const float idel = rp.inv_delta, del = rp.delta;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
     const bool inxy = act && im && ip && jm && jp;
     const unsigned nx = (unsigned)G.nx, nxy = (unsigned)G.nxy;
     const unsigned col = act ? (unsigned)j * nx + (unsigned)i : 0u;
-    const int k0 = c * CZ, k1 = min(G.nz, k0 + CZ);
+    const int k0 = c * A.CZ, k1 = min(G.nz, k0 + A.CZ);
     float* xs = upd_sm + (size_t)jj * G.nz * 33;
     float* tot = upd_sm + (size_t)blockDim.z * G.nz * 33 + (size_t)(jj * NZC) * 32;
+    const float* __restrict__ kappa = A.kappa;
     float W[4][3][3], K[4][3][3], XC[4];
     float Dv[2], Gv[2], Hv[2];  // D_L, g, htilde of the current / next voxel
     // raw loads into a ring slot; the slot is scaled by 1/delta one step later
@@ -220,12 +199,13 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
             for (int b = 0; b < 3; b++) W[S][a][b] *= idel;
     };
     auto load_vox = [&](auto par_c, int k) {
+        if (!FULL) return;
         constexpr int Q = decltype(par_c)::value;
         const bool ok = act && k < k1;
         const unsigned idx = ok ? (unsigned)k * nxy + col : 0u;
-        Dv[Q] = ok ? __ldg(dl + idx) : 0.f;
-        Gv[Q] = ok ? __ldg(g + idx) : 0.f;
-        Hv[Q] = ok ? ht[idx] : 0.f;
+        Dv[Q] = ok ? __ldg(A.dl + idx) : 0.f;
+        Gv[Q] = ok ? __ldg(A.g + idx) : 0.f;
+        Hv[Q] = ok ? A.ht[idx] : 0.f;
     };
     float run = 0.f;
     // voxel k: planes k-1, k, k+1 in slots ZA, ZB, ZC (ZC loaded raw one step
@@ -246,16 +226,21 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
             else
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
-            const float xv = XC[ZB];
-            const float d = Dv[Q], htv = Hv[Q];
-            const float s = fmaf(rho, htv, (1.f - rho) * Gv[Q]);
-            const float den = fmaf(rho, d, 2.f * cs);
-            xnew = xv;
-            if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(fmaf(del, gs, s), den), box_lo), box_hi);
-            xn[idx] = xnew;
-            ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+            if (FULL) {
+                const float xv = XC[ZB];
+                const float d = Dv[Q], htv = Hv[Q];
+                const float s = fmaf(rho, htv, (1.f - rho) * Gv[Q]);
+                const float den = fmaf(rho, d, 2.f * cs);
+                xnew = xv;
+                if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(fmaf(del, gs, s), den), A.box_lo), A.box_hi);
+                xn[idx] = xnew;
+                A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+            } else {
+                A.grad_out[idx] = del * gs;
+                if (A.curv_out) A.curv_out[idx] = 2.f * cs;
+            }
         }
-        if (pfx) {
+        if (FULL && A.pfx) {
             xs[k * 33 + lane] = xnew;
             run += xnew;
         }
@@ -279,41 +264,57 @@ __global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl
         if (k + 3 >= k1) break;
         step(I3(), I0(), I1(), I2(), k + 3);
     }
-    if (!pfx) return;
-    tot[c * 32 + lane] = run;
-    __syncthreads();
-    float P = 0.f;
-    for (int q = 0; q < c; q++) P += tot[q * 32 + lane];
-    if (!act) return;
-    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + (size_t)col * (size_t)pfx_stride_of(G);
+    if (FULL && A.pfx) write_prefix(G, A.pfx, xs, tot, run, c, lane, act, col, k0, k1);
+}
+
+// Multi-GPU sub-iteration j: folds the all-reduced zeta of
+// sub-iteration j-1 into g and htilde (Algorithm 1 lines 7-8 with rho_{j-2}),
+// then runs lines 4-5 of sub-iteration j with rho_{j-1} from grad R(x) and D_R(x)
+// computed by the UPD_STEN kernel while the all-reduce was in flight.  Elementwise
+// (same block shape and z-prefix as k_update).  Ctl.k = j - 2 on entry (the
+// advance follows this kernel); x buffers: in = A.xin, out = A.xa.
+__global__ void __launch_bounds__(256) k_update_pre(DGeom G, const Ctl* __restrict__ ctl, UpdArgs A) {
+    extern __shared__ float upd_sm[];
+    const int lane = threadIdx.x, c = threadIdx.y, jj = threadIdx.z;
+    const int NZC = blockDim.y;
+    const int i = blockIdx.x * 32 + lane;
+    const int j = blockIdx.y * blockDim.z + jj;
+    const bool act = i < G.nx && j < G.ny;
+    const float alpha = ctl->alpha;
+    const float rho_f = rho_at(ctl, ctl->k), rho = rho_at(ctl, ctl->k + 1);
+    const float inv_f = 1.f / (rho_f + 1.f);
+    const unsigned col = act ? (unsigned)j * (unsigned)G.nx + (unsigned)i : 0u;
+    const int k0 = c * A.CZ, k1 = min(G.nz, k0 + A.CZ);
+    float* xs = upd_sm + (size_t)jj * G.nz * 33;
+    float* tot = upd_sm + (size_t)blockDim.z * G.nz * 33 + (size_t)(jj * NZC) * 32;
+    float run = 0.f;
     for (int k = k0; k < k1; k++) {
-        const float xk = xs[k * 33 + lane];
-        pc[k] = make_float2(P, xk);  // (P_k, x_k): prefix before voxel k and the voxel
-        P += xk;
+        float xnew = 0.f;
+        if (act) {
+            const unsigned idx = (unsigned)k * (unsigned)G.nxy + col;
+            // lines 7-8 of sub-iteration j-1 (same arithmetic as the back-projection epilogue)
+            const float z = __ldg(A.zeta + idx), gv = A.g[idx];
+            const float gn = fmaf(rho_f * inv_f, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv_f);
+            const float htv = fmaf(alpha, z, A.ht[idx]);
+            A.g[idx] = gn;
+            // lines 4-5 of sub-iteration j
+            const float xv = __ldg(A.xin + idx), d = __ldg(A.dl + idx);
+            const float s = fmaf(rho, htv, (1.f - rho) * gn);
+            const float den = fmaf(rho, d, __ldg(A.curv + idx));
+            xnew = xv;
+            if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(__ldg(A.grad + idx) + s, den), A.box_lo), A.box_hi);
+            A.xa[idx] = xnew;
+            A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+        }
+        if (A.pfx) {
+            xs[k * 33 + lane] = xnew;
+            run += xnew;
+        }
     }
-    if (k1 == G.nz) pc[G.nz] = make_float2(P, 0.f);  // (P_nz, 0)
+    if (A.pfx) write_prefix(G, A.pfx, xs, tot, run, c, lane, act, col, k0, k1);
 }
 
-template <int POT, int NDIRS>
-static void reg_dispatch(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad,
-                         float* curv, cudaStream_t s) {
-    dim3 block(32, 8), grid((G.nx + 31) / 32, (G.ny + 7) / 8, G.nz);
-    if (kappa) k_reg<POT, NDIRS, true><<<grid, block, 0, s>>>(G, rp, x, kappa, grad, curv);
-    else k_reg<POT, NDIRS, false><<<grid, block, 0, s>>>(G, rp, x, kappa, grad, curv);
-}
-
-void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad, float* curv,
-                cudaStream_t s) {
-    const bool d4 = rp.n_dirs == 4;
-    switch (rp.potential) {
-        case 0: d4 ? reg_dispatch<0, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<0, 13>(G, rp, x, kappa, grad, curv, s); break;
-        case 1: d4 ? reg_dispatch<1, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<1, 13>(G, rp, x, kappa, grad, curv, s); break;
-        default: d4 ? reg_dispatch<2, 4>(G, rp, x, kappa, grad, curv, s) : reg_dispatch<2, 13>(G, rp, x, kappa, grad, curv, s); break;
-    }
-    launches_add(1);
-}
-
-// launch shape of k_update: NZC z-chunks of CZ voxels, JPB rows per block (<= 256 threads)
+// launch shape of the update kernels: NZC z-chunks of CZ voxels, JPB rows per block (<= 256 threads)
 struct UpdShape {
     int nzc, cz, jpb;
     size_t smem;
@@ -334,36 +335,81 @@ static UpdShape upd_shape(const DGeom& G, bool pfx) {
     return u;
 }
 
-size_t update_smem_bytes(const DGeom& G) { return upd_shape(G, true).smem; }
-
-template <int POT, int NDIRS>
-static void upd_dispatch(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
-                         const float* g, float* ht, const float* kappa, float lo, float hi, float* pfx,
-                         cudaStream_t s) {
-    static const int nopfx = env_int("CTR_UPD_NOPFX", 0);  // timing experiment only: skips the prefix
-    if (nopfx) pfx = nullptr;
-    const UpdShape u = upd_shape(G, pfx != nullptr);
+template <int POT, int NDIRS, bool KAPPA, int MODE>
+static void upd_launch(const DGeom& G, const RegParams& rp, const Ctl* ctl, UpdArgs A, cudaStream_t s) {
+    const UpdShape u = upd_shape(G, A.pfx != nullptr);
+    A.CZ = u.cz;
     dim3 block(32, u.nzc, u.jpb), grid((G.nx + 31) / 32, (G.ny + u.jpb - 1) / u.jpb, 1);
-    if (kappa) {
-        if (u.smem > 48 * 1024)
-            cudaFuncSetAttribute(k_update<POT, NDIRS, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)u.smem);
-        k_update<POT, NDIRS, true><<<grid, block, u.smem, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx, u.cz);
-    } else {
-        if (u.smem > 48 * 1024)
-            cudaFuncSetAttribute(k_update<POT, NDIRS, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)u.smem);
-        k_update<POT, NDIRS, false><<<grid, block, u.smem, s>>>(G, rp, ctl, xa, xb, dl, g, ht, kappa, lo, hi, pfx, u.cz);
+    if (u.smem > 48 * 1024)
+        cudaFuncSetAttribute(k_update<POT, NDIRS, KAPPA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)u.smem);
+    k_update<POT, NDIRS, KAPPA, MODE><<<grid, block, u.smem, s>>>(G, rp, ctl, A);
+}
+
+template <int MODE>
+static void upd_select(const DGeom& G, const RegParams& rp, const Ctl* ctl, const UpdArgs& A, cudaStream_t s) {
+    const bool d4 = rp.n_dirs == 4, kp = A.kappa != nullptr;
+#define CTR_UPD_CASE(POT)                                                              \
+    if (d4) kp ? upd_launch<POT, 4, true, MODE>(G, rp, ctl, A, s) : upd_launch<POT, 4, false, MODE>(G, rp, ctl, A, s); \
+    else kp ? upd_launch<POT, 13, true, MODE>(G, rp, ctl, A, s) : upd_launch<POT, 13, false, MODE>(G, rp, ctl, A, s);
+    switch (rp.potential) {
+        case 0: CTR_UPD_CASE(0) break;
+        case 1: CTR_UPD_CASE(1) break;
+        default: CTR_UPD_CASE(2) break;
     }
+#undef CTR_UPD_CASE
+}
+
+void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad, float* curv,
+                cudaStream_t s) {
+    UpdArgs A = {};
+    A.xin = x;
+    A.kappa = kappa;
+    A.grad_out = grad;
+    A.curv_out = curv;
+    upd_select<UPD_STEN>(G, rp, nullptr, A, s);
+    launches_add(1);
 }
 
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                    const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s) {
-    const bool d4 = rp.n_dirs == 4;
-    switch (rp.potential) {
-        case 0: d4 ? upd_dispatch<0, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<0, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
-        case 1: d4 ? upd_dispatch<1, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<1, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
-        default: d4 ? upd_dispatch<2, 4>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s) : upd_dispatch<2, 13>(G, rp, ctl, xa, xb, dl, g, ht, kappa, box_lo, box_hi, pfx, s); break;
-    }
+    static const int nopfx = env_int("CTR_UPD_NOPFX", 0);  // timing experiment only: skips the prefix
+    UpdArgs A = {};
+    A.xa = xa;
+    A.xb = xb;
+    A.dl = dl;
+    A.g = const_cast<float*>(g);
+    A.ht = ht;
+    A.kappa = kappa;
+    A.pfx = nopfx ? nullptr : pfx;
+    A.box_lo = box_lo;
+    A.box_hi = box_hi;
+    upd_select<UPD_FULL>(G, rp, ctl, A, s);
+    launches_add(1);
+}
+
+void launch_update_pre(const DGeom& G, const Ctl* ctl, const float* xin, float* xout, const float* dl, float* g,
+                       float* ht, const float* zeta, const float* grad, const float* curv, float box_lo,
+                       float box_hi, float* pfx, cudaStream_t s) {
+    UpdArgs A = {};
+    A.xin = xin;
+    A.xa = xout;
+    A.dl = dl;
+    A.g = g;
+    A.ht = ht;
+    A.zeta = zeta;
+    A.grad = grad;
+    A.curv = curv;
+    A.pfx = pfx;
+    A.box_lo = box_lo;
+    A.box_hi = box_hi;
+    const UpdShape u = upd_shape(G, pfx != nullptr);
+    A.CZ = u.cz;
+    dim3 block(32, u.nzc, u.jpb), grid((G.nx + 31) / 32, (G.ny + u.jpb - 1) / u.jpb, 1);
+    if (u.smem > 48 * 1024)
+        cudaFuncSetAttribute(k_update_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)u.smem);
+    k_update_pre<<<grid, block, u.smem, s>>>(G, ctl, A);
     launches_add(1);
 }
 

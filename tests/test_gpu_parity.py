@@ -314,22 +314,28 @@ def test_full_size_subiteration_sampled(C, name):
     assert rel(ht_gpu.ravel()[idx], hto) <= 1e-4, rel(ht_gpu.ravel()[idx], hto)
 
 
-def test_nccl_sharded_path_world1_matches_single_gpu(C):
-    """The view-sharded solve path (partial zeta -> ncclAllReduce -> g/htilde
-    kernel) on a world-1 NCCL communicator equals the fused single-GPU path."""
+@pytest.mark.parametrize("kind", ["helical_arc", "fan2d_arc"])
+def test_nccl_sharded_path_world1_matches_single_gpu(C, kind):
+    """The multi-GPU solve path (partial zeta -> ncclAllReduce overlapped with
+    the stencil of the new x on a side stream -> fold + x-update kernel) on a
+    world-1 NCCL communicator equals the fused single-GPU path, also when the
+    run is split over two calls (the last zeta is folded before returning)."""
     from paper_1512_04564_b200.recon import Recon
-    pb = synthetic_problem(tiny("helical_arc"), M=3)
+    pb = synthetic_problem(tiny(kind), M=3)
     uid = C.ct_nccl_unique_id()
     d = C.ct_dist_create(0, 1, uid, 0)
     try:
         outs = []
-        for dist in (None, d):
+        for dist, calls in ((None, (7,)), (d, (7,)), (d, (3, 4))):
             r = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], dist=dist)
             r.compute_DL()
-            r.run(7)
+            for n in calls:
+                r.run(n)
+            assert r.k == 7
             outs.append((host(r.x), host(r.g), host(r.htilde), host(r.dl)))
             r.close()
-        for a, b in zip(*outs):
-            assert rel(b, a) <= 1e-5   # same arithmetic, different FMA contraction
+        for o in outs[1:]:
+            for a, b in zip(outs[0], o):
+                assert rel(b, a) <= 1e-5   # same arithmetic, different FMA contraction / order
     finally:
         C.ct_dist_destroy(d)
