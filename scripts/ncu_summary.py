@@ -67,7 +67,7 @@ def main():
             f.write("%s,%d,%.1f,%.2f\n" % (n, c, t / 1e3, t / 1e3 / c))
     # the sub-iteration kernels of the solve (graph replays + profiled eager run)
     sub = {k: v for k, v in agg.items() if k.startswith(("k_update", "k_advance")) or
-           (k.startswith("k_fwd3") and ",1,2,1>" in k) or (k.startswith("k_back") and ",3,3,0," in k)}
+           (k.startswith("k_fwd3") and ",1,2,1>" in k) or (k.startswith("k_back3") and ",3,0," in k)}
     tot = sum(v[1] for v in sub.values())
     lines = ["# ncu summary %s" % tag, "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
@@ -88,7 +88,12 @@ def main():
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "smsp__inst_executed.sum"]
-    lines += ["", "Full capture (`ncu --set full --clock-control none`), one launch per kernel:", "",
+    urow = dict(zip(list(csv.reader(io.StringIO(subprocess.run(
+        ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)))[0],
+        list(csv.reader(io.StringIO(subprocess.run(
+            ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)))[1]))
+    lines += ["", "Full capture (`ncu --set full --clock-control none`), one launch per kernel "
+              "(units: " + ", ".join("%s [%s]" % (w, urow.get(w, "")) for w in want[:3]) + "):", "",
               "| kernel | " + " | ".join(w.split(".")[0].replace("__", ".") + ("" if "pct" not in w else " %")
                                        for w in want) + " |",
               "|---" * (len(want) + 1) + "|"]
