@@ -161,6 +161,13 @@ static DGeom make_dgeom(const ct_geom_desc* d) {
     G.inv_dt = (float)(1.0 / d->dt);
     G.dso = (float)d->dso;
     G.dsd = (float)d->dsd;
+    G.zbot = (float)(-0.5 * G.nz * d->dz + d->offset_z);
+    G.ztop = (float)(0.5 * G.nz * d->dz + d->offset_z);
+    {
+        const double ex = 0.5 * d->nx * d->dx + std::fabs(d->offset_x);
+        const double ey = 0.5 * d->ny * d->dy + std::fabs(d->offset_y);
+        G.rxy = (float)(std::sqrt(ex * ex + ey * ey) * (1.0 + 1e-6));
+    }
     G.nxy = (long long)d->nx * d->ny;
     G.nvox = G.nxy * G.nz;
     return G;

@@ -29,6 +29,8 @@ struct DGeom {
     float s_c0;           // (ns-1)/2 + offset_s: fractional column of tau = 0
     float t_c0p;          // (nt-1)/2 + offset_t + 1/2: row units, row t spans [t, t+1)
     float dt, inv_dt, dso, dsd;
+    float zbot, ztop;     // z-extent of the volume (voxel edges)
+    float rxy;            // radius of the volume's circumscribed cylinder (incl. offsets)
     long long nxy, nvox;
 };
 

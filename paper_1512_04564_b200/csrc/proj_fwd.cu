@@ -148,7 +148,9 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 // s0..s0+3 of one view (the union of their fan wedges); lane l owns the RPL
 // consecutive detector rows t = RPL*l + r of all four columns.  The warp walks
 // the union wedge 8 slabs at a time: lanes split the candidate voxel columns
-// (4 per slab per pass), evaluate their footprints in parallel (ct_footprint,
+// (4 per slab per pass), test the column's magnified axial extent against the
+// detector rows first (helical views near the ends of the helix reach few
+// rows), evaluate the transaxial footprints in parallel (ct_internal.cuh,
 // shared with the back-projector; F1 for the four detector columns) and push
 // the voxel columns with any F1 > 0 into a warp queue (ballot + prefix
 // popcount).  Each queued voxel column is resampled onto the rows once and
@@ -266,9 +268,18 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const int i = xstep ? sl : o, j = xstep ? o : sl;
                     const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
                     const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
-                    if (fmaf(nlx, cx, nly * cy) + suppl >= -tol_l && fmaf(nrx, cx, nry * cy) + suppr >= -tol_r) {
-                        Footprint f;
-                        ct_footprint<ARC>(G, cb, sb, zs, i, j, f);
+                    FpBase fb;
+                    Footprint f;
+                    bool cand = fmaf(nlx, cx, nly * cy) + suppl >= -tol_l && fmaf(nrx, cx, nry * cy) + suppr >= -tol_r;
+                    if (cand) {
+                        // axial extent first: a column whose magnified extent misses the detector
+                        // rows (helical views near the ends of the helix) is not queued
+                        fp_base(G, cb, sb, i, j, fb);
+                        fp_axial<ARC>(G, fb, zs, f.B0, f.H);
+                        cand = f.B0 < (float)G.nt && fmaf(fnz, f.H, f.B0) > 0.f;
+                    }
+                    if (cand) {
+                        fp_trans<ARC>(G, cb, sb, fb, f);
                         // F1 of the 4 detector columns from 5 edge evaluations
                         float T0 = trap_T(f, ((float)s0 - 0.5f) - f.sfc);
                         float Fc[F3_CPW];
