@@ -298,27 +298,37 @@ def run_cuda(args):
         nnz += C.ct_count_nnz(rec.h, C.views(st_, sd_, ct_))
     nnz_sub = nnz / M
 
-    # ---- e2e: through the public API with host buffers (pinned), every step
+    # ---- e2e: through the public API with host buffers (pinned), every step: step i's y, w
+    # go host->device (copy stream, double-buffered, overlapping step i-1), x of every step
+    # comes back device->host; the timed region spans the first copy to the last read-back.
     e2e = None
     if not args.no_e2e:
+        from paper_1512_04564_b200.recon import HostPipeline
         y_h = inputs["y"].cpu().pin_memory()
         w_h = inputs["w"].cpu().pin_memory()
-        x_h = torch.empty(rec.x.shape, dtype=torch.float32).pin_memory()
+        x_h = [torch.empty(rec.x.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
+        pipe = HostPipeline(rec)
+        # untimed: one cycle over both device buffers (captures the solve graph of each)
+        pipe.enqueue_copy_in(y_h, w_h)
+        pipe.step(M, x_h[0], next_inputs=(y_h, w_h))
+        pipe.step(M, x_h[1], next_inputs=None)
+        pipe.finish()
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        for _ in range(args.steps):
-            rec.y.copy_(y_h, non_blocking=True)
-            rec.w.copy_(w_h, non_blocking=True)
-            rec.run(M)
-            x_h.copy_(rec.x, non_blocking=True)
+        pipe.enqueue_copy_in(y_h, w_h)
+        for it in range(args.steps):
+            nxt = (y_h, w_h) if it + 1 < args.steps else None
+            pipe.step(M, x_h[it % 2], next_inputs=nxt)
+        pipe.finish()
         t1.record(stream)
         barrier()
         ems = max_over_ranks(t0.elapsed_time(t1))
         e2e = {"value": M * args.steps / (ems / 1000.0), "unit": "subset-iters/s",
-               "h2d_bytes_per_step": int(y_h.numel() * 4 + w_h.numel() * 4),
-               "d2h_bytes_per_step": int(x_h.numel() * 4)}
+               "h2d_bytes_per_step": int(pipe.h2d_bytes(y_h, w_h)),
+               "d2h_bytes_per_step": int(x_h[0].numel() * 4),
+               "pipelined": "host->device copy of step i+1 and read-back of step i overlap step i+1's solve"}
 
     if rank != 0:
         if world > 1:

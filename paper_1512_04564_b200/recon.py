@@ -78,3 +78,68 @@ class Recon:
             self.close()
         except Exception:
             pass
+
+
+class HostPipeline:
+    """Host-resident data through the C-ABI with the copies hidden behind the
+    solve: step i copies its (y, w) from pinned host memory into one of two
+    device buffers on a copy stream while step i-1 computes on the other, runs
+    `n_subiters` sub-iterations of `rec` on that data, snapshots x on the device
+    and reads the snapshot back to pinned host memory on the copy stream.
+    Every step moves its own inputs host->device and its result
+    device->host; only the order is pipelined.  Allocation and CUDA stream /
+    event plumbing only -- every arithmetic step is the C-ABI's."""
+
+    def __init__(self, rec):
+        self.rec = rec
+        dev = rec.dev
+        self.copy = torch.cuda.Stream(device=dev)
+        self.comp = rec.stream if rec.stream is not None else torch.cuda.current_stream(dev)
+        self.bufs = [(rec.y, rec.w), (torch.empty_like(rec.y), torch.empty_like(rec.w) if rec.w is not None else None)]
+        self.snaps = [torch.empty_like(rec.x), torch.empty_like(rec.x)]
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.used = [torch.cuda.Event(), torch.cuda.Event()]   # buffer i free again
+        self.snapped = [torch.cuda.Event(), torch.cuda.Event()]
+        self.read = [torch.cuda.Event(), torch.cuda.Event()]   # snapshot i read back
+        for e in self.used + self.read:
+            e.record(self.comp)
+        self.i = 0
+
+    def h2d_bytes(self, y_h, w_h):
+        return y_h.numel() * y_h.element_size() + (w_h.numel() * w_h.element_size() if w_h is not None else 0)
+
+    def enqueue_copy_in(self, y_h, w_h):
+        """Queue the host->device copy of the next step's inputs (buffer i % 2)."""
+        b = self.i % 2
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.used[b])
+            self.bufs[b][0].copy_(y_h, non_blocking=True)
+            if w_h is not None:
+                self.bufs[b][1].copy_(w_h, non_blocking=True)
+            self.copied[b].record(self.copy)
+
+    def step(self, n_subiters, x_h, next_inputs=None):
+        """Run step i on buffer i % 2 (its copy must have been enqueued), queue
+        the copy of `next_inputs` = (y_h, w_h) for step i+1, read x back."""
+        b = self.i % 2
+        rec = self.rec
+        self.comp.wait_event(self.copied[b])
+        rec.y, rec.w = self.bufs[b]
+        if next_inputs is not None:
+            self.i += 1
+            self.enqueue_copy_in(*next_inputs)
+            self.i -= 1
+        rec.run(n_subiters)
+        self.used[b].record(self.comp)
+        self.comp.wait_event(self.read[b])
+        self.snaps[b].copy_(rec.x)
+        self.snapped[b].record(self.comp)
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.snapped[b])
+            x_h.copy_(self.snaps[b], non_blocking=True)
+            self.read[b].record(self.copy)
+        self.i += 1
+
+    def finish(self):
+        """Make the compute stream wait for every outstanding copy."""
+        self.comp.wait_stream(self.copy)
