@@ -157,12 +157,13 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 // credited to the four detector columns with their own L = L_xy F1 (a voxel
 // column's footprint covers ~2.4 detector columns, so this removes most of the
 // redundant resampling of a one-column-per-warp walk).
-//   PFX (solve path): the x-update writes (P_k, x_k), P_k = sum_{k'<k} x_k',
-//     of every voxel column (float2, z-fastest, stride pfx_stride).  The
-//     magnified column is a piecewise-linear cumulative X(u) = H (P_k + frac x_k)
-//     over row units u, and the exact F2-weighted row sum is X(t+1) - X(t):
-//     RPL interpolations (one 8-byte gather each) per lane plus one shuffle,
-//     no per-voxel loop, no divergence.
+//   PFX (solve path): the x-update writes (M_k, x_k), M_k = P_k + x_k / 2 with
+//     P_k = sum_{k'<k} x_k', of every voxel column (float2, z-fastest, stride
+//     pfx_stride).  The magnified column is a piecewise-linear cumulative
+//     X(u) = H (P_k + frac x_k) = H (M_k + (f' - k) x_k) over row units u, and
+//     the exact F2-weighted row sum is X(t+1) - X(t): RPL interpolations (one
+//     8-byte gather each) per lane plus one shuffle, no per-voxel loop, no
+//     divergence.
 //   direct (ct_forward / init / D_L): row t loops over the voxels whose
 //     magnified extent [b_k, b_k+1] meets [t, t+1] (same overlap arithmetic as
 //     the back-projector), reading x in the boundary layout.
@@ -295,12 +296,13 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             eL = make_float4(Ls * Fc[0], Ls * Fc[1], Ls * Fc[2], Ls * Fc[3]);
                             if (PFX) {
                                 const float invH = __fdividef(1.f, f.H);
-                                const float b0 = -f.B0 * invH;
-                                // X at the top boundary RPL*32 of the lanes' rows (lane 31 needs it)
+                                // f' = (u - B0)/H - 1/2 (voxel coordinate minus 1/2); X at the top
+                                // boundary RPL*32 of the lanes' rows (lane 31 needs it)
+                                const float b0 = fmaf(-f.B0, invH, -0.5f);
                                 const float2* __restrict__ Qc =
                                     Q + (unsigned)(j * G.nx + i) * (unsigned)pfx_stride;
-                                float ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), 0.f), fnz);
-                                const float rt = __fadd_rn(__fadd_rn(ft, -0.5f), 12582912.0f);
+                                const float ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), -0.5f), fnz - 0.5f);
+                                const float rt = __fadd_rn(ft, 12582912.0f);
                                 const float2 qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
                                 const float xtop = fmaf(ft - (rt - 12582912.0f), qt.y, qt.x);
                                 eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), xtop);
@@ -324,21 +326,20 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const int col = __float_as_int(q.z);
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
-                        // X(u) = H (P_k + frac x_k) at the lane's RPL lower row boundaries; the
-                        // upper boundary of its last row is the next lane's first (shuffle),
-                        // lane 31 takes the producer's X(RPL*32).
-                        const float2* __restrict__ Qc = Q + (unsigned)col * (unsigned)pfx_stride;
+                        // X(u) = H (M_k + (f' - k) x_k), M_k = P_k + x_k / 2, f' = (u - B0)/H - 1/2,
+                        // k = round(f') (1.5*2^23 magic number; f' clamped to [-1/2, nz - 1/2],
+                        // where either rounding of a tie gives the same X: X is continuous and
+                        // Q_nz = (P_nz, 0)), at the lane's RPL lower row boundaries; the upper
+                        // boundary of its last row is the next lane's first (shuffle), lane 31
+                        // takes the producer's X(RPL*32).  Unsigned 32-bit element offsets.
+                        const unsigned cb2 = (unsigned)col * (unsigned)pfx_stride - 0x4B400000u;
                         float Xp[RPL + 1];
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
                             float f = fmaf((float)(RPL * lane + r), q.y, q.x);
-                            f = fminf(fmaxf(f, 0.f), fnz);
-                            // k = round-to-nearest(f - 1/2) via the 1.5*2^23 magic number, so
-                            // k <= f <= k+1 (at an integer f either neighbouring segment gives the
-                            // same X: X is continuous; Q_nz = (P_nz, 0)).
-                            const float rm = __fadd_rn(__fadd_rn(f, -0.5f), 12582912.0f);
-                            const int k = __float_as_int(rm) - 0x4B400000;
-                            const float2 qk = __ldg(Qc + k);
+                            f = fminf(fmaxf(f, -0.5f), fnz - 0.5f);
+                            const float rm = __fadd_rn(f, 12582912.0f);
+                            const float2 qk = __ldg(Q + (cb2 + (unsigned)__float_as_int(rm)));
                             Xp[r] = fmaf(f - (rm - 12582912.0f), qk.y, qk.x);
                         }
                         const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);
