@@ -144,8 +144,11 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 //     the boundary layout (coalesced over i); with pfx the z-prefix of x+.
 //   UPD_STEN (ct_reg_grad, and the multi-GPU path where the stencil of the new
 //     x overlaps the zeta all-reduce): grad R(x) and D_R(x) only.
+#ifndef UPD_MINB
+#define UPD_MINB 1
+#endif
 template <int POT, int NDIRS, bool KAPPA, int MODE>
-__global__ void __launch_bounds__(256) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, UpdArgs A) {
+__global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, UpdArgs A) {
     extern __shared__ float upd_sm[];  // pfx: xs[JPB][nz][33], tot[JPB][NZC][32]
     constexpr bool FULL = (MODE == UPD_FULL);
     const int lane = threadIdx.x, c = threadIdx.y, jj = threadIdx.z;
@@ -327,7 +330,7 @@ static int env_int(const char* name, int dflt) {
 
 static UpdShape upd_shape(const DGeom& G, bool pfx) {
     UpdShape u;
-    static const int zdiv = env_int("CTR_UPD_ZDIV", 32);  // tuning knob: voxels per z-chunk target
+    static const int zdiv = env_int("CTR_UPD_ZDIV", 24);  // tuning knob: voxels per z-chunk target
     u.nzc = std::min(8, std::max(1, G.nz / std::max(1, zdiv)));
     u.cz = (G.nz + u.nzc - 1) / u.nzc;
     u.nzc = (G.nz + u.cz - 1) / u.cz;
