@@ -103,6 +103,14 @@ typedef struct {
 typedef enum { OSLALM_RHO_CONTINUATION = 0, OSLALM_RHO_FIXED = 1 } oslalm_rho_mode;
 typedef enum { OSLALM_INIT_LAST_SUBSET = 0, OSLALM_INIT_FULL = 1 } oslalm_init_grad;
 
+/* Which OS-LALM recursion:
+ *   OSLALM_PROPOSED  Algorithm 1, s = rho (D_L x - h) + (1 - rho) g
+ *   OSLALM_SIMPLE    Algorithm 2, s = rho zeta + (1 - rho) g, no h
+ * alpha = 1 reverts either to the unrelaxed OS-LALM; SIMPLE with
+ * rho_mode FIXED, rho_fixed = 1 is OS-SQS [erdogan:99:osa] (s = zeta, step
+ * (D_L + D_R)^{-1}), the paper's conventional baseline. */
+typedef enum { OSLALM_PROPOSED = 0, OSLALM_SIMPLE = 1 } oslalm_variant;
+
 /* Algorithm 1 inputs ("M >= 1, 1 <= alpha < 2").  box = [box_lo, box_hi]
  * is Omega; box_hi = +inf for the non-negativity constraint. */
 typedef struct {
@@ -112,6 +120,7 @@ typedef struct {
     double rho_fixed;  /* used when rho_mode == FIXED, > 0 */
     int32_t init_grad; /* oslalm_init_grad; LAST_SUBSET = P:336 literally */
     double box_lo, box_hi;
+    int32_t variant;   /* oslalm_variant; 0 = Algorithm 1 */
 } oslalm_params;
 
 /*
@@ -122,6 +131,8 @@ typedef struct {
  *           carries htilde instead of h: the two are algebraically identical
  *           updates, but htilde avoids the float32
  *           cancellation of D_L x - h in line 4.  oslalm_state_h() recovers h.
+ *           With variant OSLALM_SIMPLE this array holds zeta, the last
+ *           subset gradient (Algorithm 2 has no h).
  *   k       number of sub-iterations done (Eq. 37 counter).  k == 0
  *           on entry runs line 1 of Alg. 1 (rho = 1, zeta = g = M grad L_M(x),
  *           h = D_L x - zeta) before the first sub-iteration.

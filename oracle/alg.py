@@ -178,13 +178,16 @@ def os_lalm_unrelaxed(prob, x0, M, iters, DL=None, rho_mode="continuation", rho_
     return x
 
 
-def os_sqs(prob, x0, M, iters, DL=None):
-    """OS-SQS [erdogan:99:osa]: x+ = [x - (D_L + D_R)^{-1}(M grad L_m(x) + grad R(x))]_+."""
+def os_sqs(prob, x0, M, iters, DL=None, first=0):
+    """OS-SQS [erdogan:99:osa] (the paper's conventional baseline):
+    x+ = [x - (D_L + D_R)^{-1}(M grad L_m(x) + grad R(x))]_+, subsets visited
+    cyclically starting at subset `first`."""
     if DL is None:
         DL = prob.D_L()
     x = np.array(x0, dtype=np.float64)
     for _ in range(iters):
-        for m in range(M):
+        for mm in range(M):
+            m = (first + mm) % M
             gradR, DR = prob.reg(x)
             x = _x_update(x, M * prob.grad_L_subset(x, m, M), gradR, DL + DR)
     return x

@@ -351,6 +351,7 @@ static ct_status validate_params(const ct_geom* g, const oslalm_params* p) {
     if (p->init_grad != OSLALM_INIT_LAST_SUBSET && p->init_grad != OSLALM_INIT_FULL)
         return fail(CT_E_CONFIG, "bad init_grad");
     if (!(p->box_lo <= p->box_hi)) return fail(CT_E_CONFIG, "box_lo > box_hi");
+    if (p->variant != OSLALM_PROPOSED && p->variant != OSLALM_SIMPLE) return fail(CT_E_CONFIG, "bad variant");
     return CT_OK;
 }
 
@@ -429,6 +430,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     h.rank = rank;
     h.world = world;
     h.rho_fixed_mode = p->rho_mode == OSLALM_RHO_FIXED;
+    h.simple = p->variant == OSLALM_SIMPLE;
     h.alpha = (float)p->alpha;
     h.rho_fixed = (float)p->rho_fixed;
     CT_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, s));
@@ -477,7 +479,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         key.ptrs = {(uintptr_t)ctl, (uintptr_t)st->x, (uintptr_t)xalt, (uintptr_t)y, (uintptr_t)w,
                     (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf,
                     (uintptr_t)xt};
-        key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi,
+        key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi, (double)p->variant,
                     (double)rp.potential, (double)rp.delta, (double)rp.n_dirs};
         for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
         std::lock_guard<std::mutex> lk(const_cast<ct_geom*>(g)->mu);

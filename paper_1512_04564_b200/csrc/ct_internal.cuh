@@ -44,6 +44,7 @@ struct Ctl {
     int M, na;
     int rank, world;    // view sharding (dist), 0/1 on a single GPU
     int rho_fixed_mode;
+    int simple;         // Algorithm 2: the htilde array holds zeta
     float alpha, rho_fixed;
     int bad;            // set by kernels on footprint overflow (debug guard)
 };

@@ -13,6 +13,7 @@
 //   BK_INIT    zeta = M A'r;  g = zeta; htilde = zeta         (line 1)
 //   BK_UPDATE  zeta = M A'r;  g = rho/(rho+1)(alpha zeta + (1-alpha) g) + g/(rho+1);
 //              htilde += alpha zeta                            (lines 6-8)
+//              (Algorithm 2, Ctl.simple: htilde = zeta)
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -67,7 +68,7 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         const float gv = gbuf[idx];
         const float inv = 1.f / (rho + 1.f);
         gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
-        htbuf[idx] = fmaf(alpha, z, htbuf[idx]);
+        htbuf[idx] = ctl->simple ? z : fmaf(alpha, z, htbuf[idx]);
     }
 }
 
@@ -248,7 +249,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 const float gv = gbuf[idx];
                 const float inv = 1.f / (rho + 1.f);
                 gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
-                htbuf[idx] = fmaf(alpha, z, htbuf[idx]);
+                htbuf[idx] = ctl->simple ? z : fmaf(alpha, z, htbuf[idx]);
             }
         }
     }

@@ -145,7 +145,7 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 //   UPD_STEN (ct_reg_grad, and the multi-GPU path where the stencil of the new
 //     x overlaps the zeta all-reduce): grad R(x) and D_R(x) only.
 #ifndef UPD_MINB
-#define UPD_MINB 1
+#define UPD_MINB 3  // <= 80 registers: 3 blocks of 256 per SM
 #endif
 template <int POT, int NDIRS, bool KAPPA, int MODE>
 __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, UpdArgs A) {
@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         rho = rho_of_k(ctl);
         alpha = ctl->alpha;
     }
+    const bool simple = FULL && ctl->simple;  // Algorithm 2: htilde holds zeta, not updated here
     const float idel = rp.inv_delta, del = rp.delta;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
     const bool inxy = act && im && ip && jm && jp;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
                 xnew = xv;
                 if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(fmaf(del, gs, s), den), A.box_lo), A.box_hi);
                 xn[idx] = xnew;
-                A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+                if (!simple) A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
             } else {
                 A.grad_out[idx] = del * gs;
                 if (A.curv_out) A.curv_out[idx] = 2.f * cs;
@@ -299,7 +300,8 @@ __global__ void __launch_bounds__(256) k_update_pre(DGeom G, const Ctl* __restri
             // lines 7-8 of sub-iteration j-1 (same arithmetic as the back-projection epilogue)
             const float z = __ldg(A.zeta + idx), gv = A.g[idx];
             const float gn = fmaf(rho_f * inv_f, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv_f);
-            const float htv = fmaf(alpha, z, A.ht[idx]);
+            const bool simple = ctl->simple;   // Algorithm 2: htilde holds zeta
+            const float htv = simple ? z : fmaf(alpha, z, A.ht[idx]);
             A.g[idx] = gn;
             // lines 4-5 of sub-iteration j
             const float xv = __ldg(A.xin + idx), d = __ldg(A.dl + idx);
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(256) k_update_pre(DGeom G, const Ctl* __restri
             xnew = xv;
             if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(__ldg(A.grad + idx) + s, den), A.box_lo), A.box_hi);
             A.xa[idx] = xnew;
-            A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
+            A.ht[idx] = simple ? htv : (1.f - alpha) * fmaf(d, xnew - xv, htv);
         }
         if (A.pfx) {
             xs[k * 33 + lane] = xnew;
@@ -425,7 +427,7 @@ __global__ void k_gh_update(long long n, const Ctl* __restrict__ ctl, const floa
          idx += (long long)gridDim.x * blockDim.x) {
         const float z = zeta[idx], gv = g[idx];
         g[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
-        ht[idx] = fmaf(alpha, z, ht[idx]);
+        ht[idx] = ctl->simple ? z : fmaf(alpha, z, ht[idx]);
     }
 }
 

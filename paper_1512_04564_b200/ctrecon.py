@@ -20,6 +20,7 @@ STATUS_NAMES = ["CT_OK", "CT_E_SHAPE", "CT_E_CONFIG", "CT_E_NUMERIC", "CT_E_DIVE
 CT_DET_FLAT, CT_DET_ARC = 0, 1
 CT_POT = {"quadratic": 0, "hyperbola": 1, "fair": 2}
 RHO_CONTINUATION, RHO_FIXED = 0, 1
+PROPOSED, SIMPLE = 0, 1   # oslalm_variant: Algorithm 1 / Algorithm 2
 INIT_LAST_SUBSET, INIT_FULL = 0, 1
 
 
@@ -54,7 +55,7 @@ class ct_reg_desc(ctypes.Structure):
 class oslalm_params(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("alpha", ctypes.c_double), ("rho_mode", ctypes.c_int32),
                 ("rho_fixed", ctypes.c_double), ("init_grad", ctypes.c_int32),
-                ("box_lo", ctypes.c_double), ("box_hi", ctypes.c_double)]
+                ("box_lo", ctypes.c_double), ("box_hi", ctypes.c_double), ("variant", ctypes.c_int32)]
 
 
 class oslalm_state(ctypes.Structure):
@@ -153,9 +154,9 @@ def reg_desc(potential, delta, betas, n_dirs):
 
 
 def params(M, alpha, rho_mode=RHO_CONTINUATION, rho_fixed=0.0, init_grad=INIT_LAST_SUBSET, box_lo=0.0,
-           box_hi=math.inf):
+           box_hi=math.inf, variant=PROPOSED):
     return oslalm_params(int(M), float(alpha), int(rho_mode), float(rho_fixed), int(init_grad), float(box_lo),
-                         float(box_hi))
+                         float(box_hi), int(variant))
 
 
 def views(start, stride, count):

@@ -36,7 +36,8 @@ class Recon:
                                C.RHO_FIXED if solver.get("rho_mode") == "fixed" else C.RHO_CONTINUATION,
                                solver.get("rho_fixed", 0.0),
                                C.INIT_FULL if solver.get("init_grad") == "full" else C.INIT_LAST_SUBSET,
-                               solver.get("box_lo", 0.0), solver.get("box_hi", math.inf))
+                               solver.get("box_lo", 0.0), solver.get("box_hi", math.inf),
+                               C.SIMPLE if solver.get("variant") == "simple" else C.PROPOSED)
         nbytes = C.oslalm_workspace_size(self.h, self.params, dist)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         self.state = C.make_state(self.x, self.g, self.htilde, 0)

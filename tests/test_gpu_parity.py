@@ -155,6 +155,40 @@ def test_solve_trace_matches_oracle(C, kind):
     rec.close()
 
 
+@pytest.mark.parametrize("kind", ["helical_arc", "fan2d_arc"])
+def test_alg2_simple_and_os_sqs_match_oracle(C, kind):
+    """Algorithm 2 (variant SIMPLE) and OS-SQS (SIMPLE with rho fixed
+    to 1) through the C-ABI against the oracle's alg2 / os_sqs."""
+    pb = synthetic_problem(tiny(kind), M=3)
+    prob = oracle_problem(pb)
+    DL = pb["DL"]
+    M, iters = 3, 2
+    xo, go = alg.alg2(prob, pb["x0"], M, 1.999, iters, DL=DL)
+    rec = _gpu_recon(dict(pb, solver=dict(pb["solver"], variant="simple")), dl=DL)
+    rec.run(M * iters)
+    assert rel(host(rec.x), xo) <= 1e-4
+    assert rel(host(rec.g), go) <= 1e-3
+    rec.close()
+    xs = alg.os_sqs(prob, pb["x0"], M, iters, DL=DL, first=M - 1)
+    rec = _gpu_recon(dict(pb, solver=dict(pb["solver"], variant="simple", rho_mode="fixed", rho_fixed=1.0)), dl=DL)
+    rec.run(M * iters)
+    assert rel(host(rec.x), xs) <= 1e-4
+    rec.close()
+
+
+def test_alpha1_alg1_equals_alg2_on_gpu(C):
+    """alpha = 1: both recursions revert to the unrelaxed OS-LALM."""
+    pb = synthetic_problem(tiny("helical_arc"), M=3, alpha=1.0)
+    outs = []
+    for variant in ("proposed", "simple"):
+        rec = _gpu_recon(dict(pb, solver=dict(pb["solver"], variant=variant)), dl=pb["DL"])
+        rec.run(7)
+        outs.append((host(rec.x), host(rec.g)))
+        rec.close()
+    assert rel(outs[1][0], outs[0][0]) <= 1e-5
+    assert rel(outs[1][1], outs[0][1]) <= 1e-5
+
+
 def test_c1_full_solve_matches_oracle(C):
     """BASELINE configs[0]: 128^2 fan, 180 views, M = 4, 20 iterations, alpha = 1.999."""
     pb = config_problem("c1")

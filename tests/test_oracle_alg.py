@@ -164,3 +164,28 @@ def test_converges_to_dense_pwls_minimiser():
                 break
         assert np.linalg.norm(x.ravel() - xhat) <= 1e-8 * np.linalg.norm(xhat), alpha
     assert reach[1.999] < reach[1.0], reach
+
+
+# ------------------------------------------------------------------ P7d (Alg. 2 / OS-SQS)
+def test_os_sqs_monotone_descent_and_alg2_rho1_is_os_sqs():
+    """OS-SQS with one subset is a majorize-minimize step (D_L majorizes A'WA,
+    P5; the Huber D_R majorizes R, P6), so the PWLS cost (Eq. 34) cannot rise;
+    Algorithm 2 with rho fixed to 1 (s = zeta) is OS-SQS with the subsets
+    visited from M-1 (its zeta is the previous subset's gradient at x)."""
+    prob, x0, _ = tiny_problem("helical_arc")
+    DL = prob.D_L()
+    x = x0.copy()
+    c_prev = prob.cost(x)
+    for _ in range(12):
+        x = alg.os_sqs(prob, x, 1, 1, DL=DL)
+        c = prob.cost(x)
+        assert c <= c_prev * (1 + 1e-13), (c, c_prev)
+        c_prev = c
+    assert c_prev < 0.99 * prob.cost(x0)
+    M, iters = 3, 4
+    for alpha in (1.0, 1.999):       # g is unused when rho = 1
+        x2 = alg.alg2(prob, x0, M, alpha, iters, DL=DL, rho_mode="fixed", rho_fixed=1.0)[0]
+        xs = alg.os_sqs(prob, x0, M, iters, DL=DL, first=M - 1)
+        assert np.linalg.norm(x2 - xs) <= 1e-12 * np.linalg.norm(xs), alpha
+    # a different visiting order gives different iterates (the pin is not vacuous)
+    assert np.linalg.norm(alg.os_sqs(prob, x0, M, iters, DL=DL) - xs) > 1e-8 * np.linalg.norm(xs)
