@@ -115,11 +115,17 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[8], c
 //      piecewise-linear cumulative R(u) = cs_o + frac rs_o (one 8-byte shared
 //      load per voxel boundary, magic-number floor).
 template <bool ARC, int EPI, bool LZ, int BK_KZ>
-__global__ void __launch_bounds__(BK_BS, BK_KZ <= 16 ? 7 : BK_KZ <= 24 ? 4 : 3)
+#ifndef BK_RM24
+#define BK_RM24 40     // rows buffered per pass at KZ = 24 (41 x 128 float2 = 42 KB)
+#endif
+#ifndef BK_MINB24
+#define BK_MINB24 5    // resident blocks per SM at KZ = 24 (<= 102 registers)
+#endif
+__global__ void __launch_bounds__(BK_BS, BK_KZ <= 16 ? 7 : BK_KZ <= 24 ? BK_MINB24 : 3)
 k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
-    constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : 44;
+    constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : BK_KZ <= 24 ? BK_RM24 : 44;
     __shared__ float2 csb[RM + 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;

@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctrecon.so")
+# CTR_LIB_PATH: load another build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("CTR_LIB_PATH") or os.path.join(_HERE, "libctrecon.so")
 
 CT_OK, CT_E_SHAPE, CT_E_CONFIG, CT_E_NUMERIC, CT_E_DIVERGED, CT_E_CUDA, CT_E_NCCL, CT_E_NOMEM = range(8)
 STATUS_NAMES = ["CT_OK", "CT_E_SHAPE", "CT_E_CONFIG", "CT_E_NUMERIC", "CT_E_DIVERGED", "CT_E_CUDA",
