@@ -170,13 +170,19 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 // No atomics; row sums live in registers; the epilogue stages the block's 32
 // detector columns through shared memory so y/w reads and r writes are
 // 128-byte runs.
-constexpr int F3_WARPS = 8;
+#ifndef F3_NWARPS
+#define F3_NWARPS 4    // warps per block (4 detector columns each)
+#endif
+#ifndef F3_SUB
+#define F3_SUB 1       // lanes per slab in the candidate walk (32 / F3_SUB slabs per pass)
+#endif
+constexpr int F3_WARPS = F3_NWARPS;
 constexpr int F3_CPW = 4;
 constexpr int F3_BS = 32 * F3_WARPS;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
 #ifndef F3_MINB
-#define F3_MINB 4  // 64 registers: 4 blocks (32 warps) per SM to hide the prefix-gather latency
+#define F3_MINB 8  // 64 registers: 8 blocks of 4 warps per SM to hide the prefix-gather latency
 #endif
 template <bool ARC, int MODE, int RPL, bool PFX>
 __global__ void __launch_bounds__(F3_BS, F3_MINB)
@@ -243,8 +249,8 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         const float inv_do = 1.f / dob;
         const float fnz = (float)G.nz;
 
-        for (int sl0 = 0; sl0 < na_; sl0 += 8) {
-            const int sl = sl0 + (lane >> 2), sub = lane & 3;
+        for (int sl0 = 0; sl0 < na_; sl0 += 32 / F3_SUB) {
+            const int sl = sl0 + lane / F3_SUB, sub = lane % F3_SUB;
             int lo = 0, hi = -1;
             if (sl < na_) {
                 const float ac = fmaf((float)sl, da, a0);
@@ -260,9 +266,9 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     }
                 }
             }
-            const int npass = __reduce_max_sync(0xffffffffu, (hi - lo + 1 + 3) >> 2);
+            const int npass = __reduce_max_sync(0xffffffffu, (hi - lo + F3_SUB) / F3_SUB);
             for (int p = 0; p < npass; p++) {
-                const int o = lo + sub + 4 * p;
+                const int o = lo + sub + F3_SUB * p;
                 bool nz = false;
                 float4 eL = make_float4(0.f, 0.f, 0.f, 0.f), eG = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (o <= hi) {
