@@ -20,7 +20,10 @@
 
 namespace ctr {
 
-constexpr int BK_Y = 4;
+#ifndef BK_YDIM
+#define BK_YDIM 4      // voxel-column rows per block (block = 32 x BK_Y threads)
+#endif
+constexpr int BK_Y = BK_YDIM;
 constexpr int BK_BS = 32 * BK_Y;
 constexpr int BK_KZ_DEFAULT = 24;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24 | 32)
 constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 at KZ = 16 (more rows => several passes)

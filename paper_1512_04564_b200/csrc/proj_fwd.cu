@@ -23,10 +23,15 @@ namespace ctr {
 // back-projector), F1 of the 8 cells from 9 edge evaluations of the trapezoid
 // antiderivative, and accumulate L_xy F1 x into 8 per-lane registers.  A warp
 // reduction forms the 8 sums; no atomics, no shared memory.
+#ifndef F2_SPLIT_W
+#define F2_SPLIT_W 4   // warps sharing one 8-cell group (each walks every F2_SPLIT-th slab batch)
+#endif
 constexpr int F2_CPW = 8;
 constexpr int F2_SUB = 8;            // lanes per slab
 constexpr int F2_SPP = 32 / F2_SUB;  // slabs per pass
 constexpr int F2_WARPS = 4;
+constexpr int F2_SPLIT = F2_SPLIT_W;
+constexpr int F2_GPB = F2_WARPS / F2_SPLIT;   // cell groups per block
 
 template <bool ARC, int MODE>
 __global__ void __launch_bounds__(32 * F2_WARPS)
@@ -39,8 +44,9 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const int vi = blockIdx.y;
     if (vi >= V.count) return;
     const int v = V.start + vi * V.stride;
-    const int s0 = (blockIdx.x * F2_WARPS + wid) * F2_CPW;
-    if (s0 >= G.ns) return;  // warp-uniform
+    const int grp = wid / F2_SPLIT, part = wid % F2_SPLIT;   // cell group, slab-batch residue
+    const int s0 = (blockIdx.x * F2_GPB + grp) * F2_CPW;
+    __shared__ float red[F2_WARPS][F2_CPW];
     const float* __restrict__ x = xa;
     if (ctl) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
     const float4 vw = __ldg(&vtab[v]);
@@ -84,7 +90,7 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
     const float inv_do = 1.f / dob;
 
-    for (int sl0 = 0; sl0 < na_; sl0 += F2_SPP) {
+    for (int sl0 = part * F2_SPP; s0 < G.ns && sl0 < na_; sl0 += F2_SPP * F2_SPLIT) {
         const int sl = sl0 + lane / F2_SUB, sub = lane % F2_SUB;
         int lo = 0, hi = -1;
         if (sl < na_) {
@@ -126,9 +132,17 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
     }
-    float q = acc[0];
+    // sum the F2_SPLIT warps of the cell group (fixed order: deterministic)
+    if (lane == 0) {
 #pragma unroll
-    for (int c = 1; c < F2_CPW; c++) q = (lane == c) ? acc[c] : q;
+        for (int c = 0; c < F2_CPW; c++) red[wid][c] = acc[c];
+    }
+    __syncthreads();
+    if (part != 0 || s0 >= G.ns) return;
+    float q = 0.f;
+    if (lane < F2_CPW) {
+        for (int pw = 0; pw < F2_SPLIT; pw++) q += red[grp * F2_SPLIT + pw][lane];
+    }
     const int s = s0 + lane;
     if (lane < F2_CPW && s < G.ns) {
         const size_t o = (size_t)vi * G.ns + s;
@@ -443,7 +457,7 @@ template <bool ARC>
 static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                           const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
                           cudaStream_t s) {
-    dim3 grid((G.ns + F2_CPW * F2_WARPS - 1) / (F2_CPW * F2_WARPS), max_count);
+    dim3 grid((G.ns + F2_CPW * F2_GPB - 1) / (F2_CPW * F2_GPB), max_count);
     const int bs = 32 * F2_WARPS;
     if (mode == FWD_PLAIN) k_fwd2<ARC, FWD_PLAIN><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
     else if (mode == FWD_RESID) k_fwd2<ARC, FWD_RESID><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
