@@ -95,7 +95,7 @@ CONFIGS = {
 }
 
 # beta0 written by scripts/calibrate_beta.py (oracle-only); see module doc.
-_BETA0 = {"c1": 3.744e5, "c2": 4.539e7, "c3": 3.278e6, "c4": 1.512e7, "c5": None}
+_BETA0 = {"c1": 3.744e5, "c2": 4.539e7, "c3": 3.278e6, "c4": 1.512e7, "c5": 1.746e6}
 
 
 def get_config(name):
