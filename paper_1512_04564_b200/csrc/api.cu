@@ -168,6 +168,8 @@ static DGeom make_dgeom(const ct_geom_desc* d) {
         const double ey = 0.5 * d->ny * d->dy + std::fabs(d->offset_y);
         G.rxy = (float)(std::sqrt(ex * ex + ey * ey) * (1.0 + 1e-6));
     }
+    G.zs0 = (float)(d->dim == 3 ? d->source_z0 : 0.0);
+    G.zstep = (float)(d->dim == 3 ? d->pitch * d->nt * d->dt * d->dso / d->dsd * (d->orbit_deg / 360.0) / d->na : 0.0);
     G.nxy = (long long)d->nx * d->ny;
     G.nvox = G.nxy * G.nz;
     return G;

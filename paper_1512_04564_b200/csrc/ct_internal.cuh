@@ -31,6 +31,7 @@ struct DGeom {
     float dt, inv_dt, dso, dsd;
     float zbot, ztop;     // z-extent of the volume (voxel edges)
     float rxy;            // radius of the volume's circumscribed cylinder (incl. offsets)
+    float zs0, zstep;     // source z of view v: zs0 + v zstep (helical; zstep = 0 axial)
     long long nxy, nvox;
 };
 

@@ -144,7 +144,27 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
 #pragma unroll
     for (int q = 0; q < BK_KZ; q++) acc[q] = 0.f;
 
-    for (int vi = 0; vi < V.count; vi++) {
+    // Helical view window of the block's z-chunk: the chunk [zlo, zhi] can reach the
+    // detector rows [0, nt) only if zlo - (nt - tc)/m < z_s < zhi + tc/m for some
+    // magnification m in [Dsd / (dso + rxy), Dsd / (dso - rxy)] / dt (row units, tc the
+    // row of z = z_s), so views whose source z is outside that window (plus a 1 mm /
+    // 1 view margin) are skipped for the whole block before the per-column test below.
+    int vi0 = 0, vi1 = V.count;
+    if (G.zstep != 0.f && V.count > 0) {
+        const float mlo = G.dsd / (G.dso + G.rxy) * G.inv_dt, mhi = G.dsd / (G.dso - G.rxy) * G.inv_dt;
+        const float zlo = G.zbot + (float)k0 * G.dz, zhi = zlo + fkz * G.dz;
+        const float up = (float)nt - G.t_c0p;   // rows above / below the row of z = z_s
+        const float wlo = zlo - fmaxf(up / mlo, up / mhi) - 1.f;
+        const float whi = zhi + fmaxf(G.t_c0p / mlo, G.t_c0p / mhi) + 1.f;
+        // z_s(v_i) = zs0 + (start + i stride) zstep, monotone in i
+        const float a = G.zs0 + (float)V.start * G.zstep, b = (float)V.stride * G.zstep;
+        float ia = (wlo - a) / b, ib = (whi - a) / b;
+        if (ia > ib) { const float t = ia; ia = ib; ib = t; }
+        vi0 = max(vi0, (int)floorf(ia) - 1);
+        vi1 = min(vi1, (int)ceilf(ib) + 2);
+    }
+
+    for (int vi = vi0; vi < vi1; vi++) {
         const int v = V.start + vi * V.stride;
         const float4 vw = __ldg(&vtab[v]);
         FpBase fb;
