@@ -178,20 +178,38 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     const float* __restrict__ kappa = A.kappa;
     float W[4][3][3], K[4][3][3], XC[4];
     float Dv[2], Gv[2], Hv[2];  // D_L, g, htilde of the current / next voxel
-    // raw loads into a ring slot; the slot is scaled by 1/delta one step later
+    // raw loads into a ring slot; the slot is scaled by 1/delta one step later.
+    // Interior columns load the 3x3 block unconditionally from a clamped plane (a
+    // plane outside the volume is never weighted: the stencil checks km/kp there).
     auto load_plane = [&](auto slot_c, int k) {
         constexpr int S = decltype(slot_c)::value;
-        const bool ok = act && k >= 0 && k < G.nz;
-        const unsigned o = ok ? (unsigned)k * nxy + col : 0u;
+        if (inxy) {
+            const int kc = min(max(k, 0), G.nz - 1);
+            const float* __restrict__ p = x + ((unsigned)kc * nxy + col - nx - 1u);
+            const float* __restrict__ pk = KAPPA ? kappa + ((unsigned)kc * nxy + col - nx - 1u) : nullptr;
 #pragma unroll
-        for (int dy = -1; dy <= 1; dy++) {
-            const bool vy = inxy || (dy < 0 ? jm : (dy > 0 ? jp : true));
-            const unsigned ro = o + (unsigned)(dy * (int)nx);
+            for (int dy = 0; dy < 3; dy++) {
 #pragma unroll
-            for (int dx = -1; dx <= 1; dx++) {
-                const bool v = ok && vy && (inxy || (dx < 0 ? im : (dx > 0 ? ip : true)));
-                W[S][dy + 1][dx + 1] = v ? __ldg(x + (ro + (unsigned)dx)) : 0.f;
-                if (KAPPA) K[S][dy + 1][dx + 1] = v ? __ldg(kappa + (ro + (unsigned)dx)) : 0.f;
+                for (int dx = 0; dx < 3; dx++) {
+                    W[S][dy][dx] = __ldg(p + dx);
+                    if (KAPPA) K[S][dy][dx] = __ldg(pk + dx);
+                }
+                p += nx;
+                if (KAPPA) pk += nx;
+            }
+        } else {
+            const bool ok = act && k >= 0 && k < G.nz;
+            const unsigned o = ok ? (unsigned)k * nxy + col : 0u;
+#pragma unroll
+            for (int dy = -1; dy <= 1; dy++) {
+                const bool vy = dy < 0 ? jm : (dy > 0 ? jp : true);
+                const unsigned ro = o + (unsigned)(dy * (int)nx);
+#pragma unroll
+                for (int dx = -1; dx <= 1; dx++) {
+                    const bool v = ok && vy && (dx < 0 ? im : (dx > 0 ? ip : true));
+                    W[S][dy + 1][dx + 1] = v ? __ldg(x + (ro + (unsigned)dx)) : 0.f;
+                    if (KAPPA) K[S][dy + 1][dx + 1] = v ? __ldg(kappa + (ro + (unsigned)dx)) : 0.f;
+                }
             }
         }
     };
@@ -206,11 +224,10 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     auto load_vox = [&](auto par_c, int k) {
         if (!FULL) return;
         constexpr int Q = decltype(par_c)::value;
-        const bool ok = act && k < k1;
-        const unsigned idx = ok ? (unsigned)k * nxy + col : 0u;
-        Dv[Q] = ok ? __ldg(A.dl + idx) : 0.f;
-        Gv[Q] = ok ? __ldg(A.g + idx) : 0.f;
-        Hv[Q] = ok ? A.ht[idx] : 0.f;
+        const unsigned idx = (unsigned)min(k, k1 - 1) * nxy + col;   // past the chunk: never used
+        Dv[Q] = __ldg(A.dl + idx);
+        Gv[Q] = __ldg(A.g + idx);
+        Hv[Q] = A.ht[idx];
     };
     float run = 0.f;
     // voxel k: planes k-1, k, k+1 in slots ZA, ZB, ZC (ZC loaded raw one step
