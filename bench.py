@@ -246,6 +246,10 @@ def run_cuda(args):
         uid = [C.ct_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         cdist = C.ct_dist_create(rank, world, uid[0], local)
+    elif args.dist_path:
+        # the multi-GPU solve path (partial zeta -> ncclAllReduce || stencil -> fold + update)
+        # on a world-1 communicator: measures its overhead against the fused 1-GPU path
+        cdist = C.ct_dist_create(0, 1, C.ct_nccl_unique_id(), local)
 
     stream = torch.cuda.current_stream(dev)
     rec = Recon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], device=local,
@@ -394,7 +398,8 @@ def run_cuda(args):
         "config": {"workload": WORKLOADS[args.config], "config": args.config, "subsets": M,
                    "sub_iters_per_step": M, "volume": list(rec.x.shape), "views": g["na"],
                    "parallelism": "views of each subset sharded over %d GPU(s), NCCL all-reduce of zeta" % world
-                   if world > 1 else "1 GPU",
+                   if world > 1 else ("1 GPU, multi-GPU code path on a world-1 NCCL communicator"
+                                      if cdist is not None else "1 GPU"),
                    "l2": "no flush: per-sub-iteration working set %.0f MB > 126 MB L2" % work_mb},
         "roofline": roof, "kernels": kernels, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks,
@@ -413,6 +418,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-path", action="store_true",
+                    help="N=1 only: run the multi-GPU code path on a world-1 NCCL communicator")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     args = ap.parse_args()
