@@ -90,14 +90,23 @@ typedef struct {
  *   0 (1,0,0) 1 (0,1,0) 2 (1,1,0) 3 (1,-1,0) 4 (0,0,1) 5 (1,0,1) 6 (-1,0,1)
  *   7 (0,1,1) 8 (0,-1,1) 9 (1,1,1) 10 (-1,1,1) 11 (1,-1,1) 12 (-1,-1,1)
  * Potentials: quadratic t^2/2; hyperbola delta^2(sqrt(1+(t/delta)^2)-1);
- * Fair delta^2(|t/delta| - log(1+|t/delta|)).  delta > 0. */
-typedef enum { CT_POT_QUADRATIC = 0, CT_POT_HYPERBOLA = 1, CT_POT_FAIR = 2 } ct_potential;
+ * Fair delta^2(|t/delta| - log(1+|t/delta|)); q-GGMRF with p = 2,
+ * (t^2/2)/(1 + |t/delta|^(2-q)), 1 <= q <= 2 (Thibault et al. 2007, the
+ * chest experiment's regulariser).  delta > 0.
+ * Curvature D_R: CT_CURV_HUBER = 2 sum beta kappa kappa
+ * omega(x_j - x_n), omega = phi'(t)/t (Huber's curvature, the paper's
+ * choice); CT_CURV_MAX = 2 sum beta kappa kappa omega(0), the maximum
+ * curvature (the constant majorizer the paper's theorems assume). */
+typedef enum { CT_POT_QUADRATIC = 0, CT_POT_HYPERBOLA = 1, CT_POT_FAIR = 2, CT_POT_QGGMRF = 3 } ct_potential;
+typedef enum { CT_CURV_HUBER = 0, CT_CURV_MAX = 1 } ct_curvature;
 
 typedef struct {
     int32_t potential; /* ct_potential */
     double delta;
     int32_t n_dirs;    /* 4 or 13 */
     double beta[13];   /* beta_i >= 0 */
+    int32_t curvature; /* ct_curvature */
+    double q;          /* q-GGMRF exponent, 1 <= q <= 2 (ignored by the other potentials) */
 } ct_reg_desc;
 
 typedef enum { OSLALM_RHO_CONTINUATION = 0, OSLALM_RHO_FIXED = 1 } oslalm_rho_mode;

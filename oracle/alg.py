@@ -40,7 +40,7 @@ def subset_rows(arr, na, M, m):
 class Problem:
     """PWLS CT problem of Eq. 34 with R of Eq. 35."""
 
-    def __init__(self, geom, y, w, potential, delta, betas, n_dirs, kappa=None):
+    def __init__(self, geom, y, w, potential, delta, betas, n_dirs, kappa=None, q=1.2, curvature="huber"):
         self.g = geom
         self.y = np.asarray(y, dtype=np.float64)
         self.w = np.asarray(w, dtype=np.float64)
@@ -49,15 +49,18 @@ class Problem:
         self.betas = list(betas)
         self.n_dirs = int(n_dirs)
         self.kappa = kappa
+        self.q = float(q)                # q-GGMRF exponent (potential "qggmrf")
+        self.curvature = curvature       # D_R: "huber" or "max"
         self.n_fwd = 0   # work accounting ("only once per iteration")
         self.n_back = 0
 
     def reg(self, x):
-        _, gr, cv = P.reg(self.g, self.potential, self.delta, self.betas, self.n_dirs, x, self.kappa)
+        _, gr, cv = P.reg(self.g, self.potential, self.delta, self.betas, self.n_dirs, x, self.kappa, q=self.q,
+                          curvature=self.curvature)
         return gr, cv
 
     def reg_value(self, x):
-        v, _, _ = P.reg(self.g, self.potential, self.delta, self.betas, self.n_dirs, x, self.kappa,
+        v, _, _ = P.reg(self.g, self.potential, self.delta, self.betas, self.n_dirs, x, self.kappa, q=self.q,
                         want_grad=False, want_curv=False)
         return v
 

@@ -53,10 +53,10 @@ def lib():
         _lib.og_back.argtypes = [P(OGeom), P(d), i, i, i, P(d)]
         _lib.og_forward_rays.argtypes = [P(OGeom), P(d), i, P(i), P(i), P(i), P(d)]
         _lib.og_back_voxels.argtypes = [P(OGeom), P(d), i, i, i, i, P(ctypes.c_int64), P(d)]
-        _lib.og_reg.argtypes = [P(OGeom), i, d, P(d), i, P(d), ctypes.c_void_p, ctypes.c_void_p,
+        _lib.og_reg.argtypes = [P(OGeom), i, d, d, i, P(d), i, P(d), ctypes.c_void_p, ctypes.c_void_p,
                                 ctypes.c_void_p]
         _lib.og_reg.restype = d
-        _lib.og_reg_at.argtypes = [P(OGeom), i, d, P(d), i, P(d), ctypes.c_void_p, i,
+        _lib.og_reg_at.argtypes = [P(OGeom), i, d, d, i, P(d), i, P(d), ctypes.c_void_p, i,
                                    P(ctypes.c_int64), P(d), P(d)]
         _lib.og_directions.argtypes = [P(i)]
         _lib.og_set_threads.argtypes = [i]
@@ -146,7 +146,8 @@ def back_voxels(g, proj, views, idx):
     return out
 
 
-POTENTIALS = {"quadratic": 0, "hyperbola": 1, "fair": 2}
+POTENTIALS = {"quadratic": 0, "hyperbola": 1, "fair": 2, "qggmrf": 3}
+CURVATURES = {"huber": 0, "max": 1}
 
 
 def _betas13(betas):
@@ -162,8 +163,10 @@ def directions():
     return [tuple(arr[3 * d:3 * d + 3]) for d in range(13)]
 
 
-def reg(g, potential, delta, betas, n_dirs, x, kappa=None, want_grad=True, want_curv=True):
-    """Return (R(x), grad, curv) of Eq. 35 with the Huber curvature (x2 SQS split)."""
+def reg(g, potential, delta, betas, n_dirs, x, kappa=None, want_grad=True, want_curv=True, q=1.2,
+        curvature="huber"):
+    """Return (R(x), grad, curv) of Eq. 35 with the Huber curvature (x2 SQS split), or the
+    maximum curvature (curvature="max"); q is the q-GGMRF exponent (potential "qggmrf")."""
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(vol_shape(g))
     b = _betas13(betas)
     grad = np.zeros_like(x) if want_grad else None
@@ -172,14 +175,15 @@ def reg(g, potential, delta, betas, n_dirs, x, kappa=None, want_grad=True, want_
     if kappa is not None:
         kap = np.ascontiguousarray(kappa, dtype=np.float64).reshape(vol_shape(g))
     G = ogeom(g)
-    val = lib().og_reg(ctypes.byref(G), POTENTIALS[potential], float(delta), _p(b), int(n_dirs), _p(x),
+    val = lib().og_reg(ctypes.byref(G), POTENTIALS[potential], float(delta), float(q), CURVATURES[curvature],
+                       _p(b), int(n_dirs), _p(x),
                        kap.ctypes.data if kap is not None else None,
                        grad.ctypes.data if grad is not None else None,
                        curv.ctypes.data if curv is not None else None)
     return val, grad, curv
 
 
-def reg_at(g, potential, delta, betas, n_dirs, x, idx, kappa=None):
+def reg_at(g, potential, delta, betas, n_dirs, x, idx, kappa=None, q=1.2, curvature="huber"):
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(vol_shape(g))
     b = _betas13(betas)
     idx = np.ascontiguousarray(idx, dtype=np.int64)
@@ -189,7 +193,8 @@ def reg_at(g, potential, delta, betas, n_dirs, x, idx, kappa=None):
     if kappa is not None:
         kap = np.ascontiguousarray(kappa, dtype=np.float64).reshape(vol_shape(g))
     G = ogeom(g)
-    lib().og_reg_at(ctypes.byref(G), POTENTIALS[potential], float(delta), _p(b), int(n_dirs), _p(x),
+    lib().og_reg_at(ctypes.byref(G), POTENTIALS[potential], float(delta), float(q), CURVATURES[curvature],
+                    _p(b), int(n_dirs), _p(x),
                     kap.ctypes.data if kap is not None else None, idx.size, _p(idx, ctypes.c_int64),
                     _p(grad), _p(curv))
     return grad, curv

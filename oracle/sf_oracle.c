@@ -334,14 +334,24 @@ static const int OG_DIRS[13][3] = {
 
 void og_directions(int* out39) { memcpy(out39, OG_DIRS, sizeof(OG_DIRS)); }
 
-/* potential 0 = quadratic, 1 = hyperbola, 2 = Fair: phi, phi', omega = phi'/t */
-static void og_pot(int pot, double delta, double t, double* phi, double* dphi, double* om) {
+/* potential 0 = quadratic, 1 = hyperbola, 2 = Fair, 3 = q-GGMRF with p = 2
+ * (Thibault et al. 2007, the chest experiment's regulariser):
+ * phi(t) = (t^2/2) / (1 + |t/delta|^(2-q)); returns phi, phi', omega = phi'/t. */
+static void og_pot(int pot, double delta, double q, double t, double* phi, double* dphi, double* om) {
     if (pot == 0) { *phi = 0.5 * t * t; *dphi = t; *om = 1.0; return; }
     if (pot == 1) {
-        double q = sqrt(1.0 + (t / delta) * (t / delta));
-        *phi = delta * delta * (q - 1.0);
-        *dphi = t / q;
-        *om = 1.0 / q;
+        double r = sqrt(1.0 + (t / delta) * (t / delta));
+        *phi = delta * delta * (r - 1.0);
+        *dphi = t / r;
+        *om = 1.0 / r;
+        return;
+    }
+    if (pot == 3) {
+        /* d/dt [t^2/2 / (1+u)], u = |t/delta|^(2-q):  t (2 + q u) / (2 (1+u)^2) */
+        double u = pow(fabs(t) / delta, 2.0 - q);
+        *phi = 0.5 * t * t / (1.0 + u);
+        *om = (2.0 + q * u) / (2.0 * (1.0 + u) * (1.0 + u));
+        *dphi = t * *om;
         return;
     }
     double a = fabs(t) / delta;
@@ -350,8 +360,11 @@ static void og_pot(int pot, double delta, double t, double* phi, double* dphi, d
     *om = 1.0 / (1.0 + a);
 }
 
-static void og_reg_voxel(const og_geom* g, int pot, double delta, const double* beta, int ndirs, const double* x,
-                         const double* kappa, int i, int j, int k, double* gr, double* cv) {
+/* curvature: D_R_j = 2 sum beta kappa kappa omega(x_j - x_n) (Huber, maxcurv = 0) or with
+ * omega(0) = 1, the maximum curvature of every potential here (maxcurv = 1). */
+static void og_reg_voxel(const og_geom* g, int pot, double delta, double q, int maxcurv, const double* beta,
+                         int ndirs, const double* x, const double* kappa, int i, int j, int k, double* gr,
+                         double* cv) {
     int nz = g->dim == 3 ? g->nz : 1;
     size_t nxy = (size_t)g->nx * g->ny;
     size_t me = (size_t)k * nxy + (size_t)j * g->nx + i;
@@ -364,9 +377,9 @@ static void og_reg_voxel(const og_geom* g, int pot, double delta, const double* 
             size_t nb = (size_t)nk * nxy + (size_t)nj * g->nx + ni;
             double kn = kappa ? kappa[nb] : 1.0;
             double phi, dphi, om;
-            og_pot(pot, delta, x[me] - x[nb], &phi, &dphi, &om);
+            og_pot(pot, delta, q, x[me] - x[nb], &phi, &dphi, &om);
             sg += beta[d] * kj * kn * dphi;
-            sc += 2.0 * beta[d] * kj * kn * om;
+            sc += 2.0 * beta[d] * kj * kn * (maxcurv ? 1.0 : om);
         }
     }
     *gr = sg;
@@ -374,8 +387,8 @@ static void og_reg_voxel(const og_geom* g, int pot, double delta, const double* 
 }
 
 /* grad = nabla R(x), curv = Huber curvature D_R (may be NULL); returns R(x). */
-double og_reg(const og_geom* g, int pot, double delta, const double* beta, int ndirs, const double* x,
-              const double* kappa, double* grad, double* curv) {
+double og_reg(const og_geom* g, int pot, double delta, double q, int maxcurv, const double* beta, int ndirs,
+              const double* x, const double* kappa, double* grad, double* curv) {
     int nz = g->dim == 3 ? g->nz : 1;
     size_t nxy = (size_t)g->nx * g->ny;
     double val = 0.0;
@@ -385,7 +398,7 @@ double og_reg(const og_geom* g, int pot, double delta, const double* beta, int n
             for (int i = 0; i < g->nx; i++) {
                 size_t me = (size_t)k * nxy + (size_t)j * g->nx + i;
                 double gr, cv;
-                og_reg_voxel(g, pot, delta, beta, ndirs, x, kappa, i, j, k, &gr, &cv);
+                og_reg_voxel(g, pot, delta, q, maxcurv, beta, ndirs, x, kappa, i, j, k, &gr, &cv);
                 if (grad) grad[me] = gr;
                 if (curv) curv[me] = cv;
                 /* value: each unordered pair once (forward directions only) */
@@ -396,7 +409,7 @@ double og_reg(const og_geom* g, int pot, double delta, const double* beta, int n
                     size_t nb = (size_t)nk * nxy + (size_t)nj * g->nx + ni;
                     double kn = kappa ? kappa[nb] : 1.0;
                     double phi, dphi, om;
-                    og_pot(pot, delta, x[me] - x[nb], &phi, &dphi, &om);
+                    og_pot(pot, delta, q, x[me] - x[nb], &phi, &dphi, &om);
                     val += beta[d] * kj * kn * phi;
                 }
             }
@@ -406,14 +419,15 @@ double og_reg(const og_geom* g, int pot, double delta, const double* beta, int n
 }
 
 /* regulariser gradient / curvature at sampled flat voxel indices */
-void og_reg_at(const og_geom* g, int pot, double delta, const double* beta, int ndirs, const double* x,
-               const double* kappa, int n, const int64_t* idx, double* grad, double* curv) {
+void og_reg_at(const og_geom* g, int pot, double delta, double q, int maxcurv, const double* beta, int ndirs,
+               const double* x, const double* kappa, int n, const int64_t* idx, double* grad, double* curv) {
     size_t nxy = (size_t)g->nx * g->ny;
     #pragma omp parallel for schedule(static)
-    for (int q = 0; q < n; q++) {
-        int k = (int)(idx[q] / (int64_t)nxy);
-        int col = (int)(idx[q] % (int64_t)nxy);
-        og_reg_voxel(g, pot, delta, beta, ndirs, x, kappa, col % g->nx, col / g->nx, k, &grad[q], &curv[q]);
+    for (int e = 0; e < n; e++) {
+        int k = (int)(idx[e] / (int64_t)nxy);
+        int col = (int)(idx[e] % (int64_t)nxy);
+        og_reg_voxel(g, pot, delta, q, maxcurv, beta, ndirs, x, kappa, col % g->nx, col / g->nx, k, &grad[e],
+                     &curv[e]);
     }
 }
 

@@ -282,7 +282,10 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
 
 static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp) {
     if (!r) return fail(CT_E_CONFIG, "ct_reg_desc is NULL");
-    if (r->potential < 0 || r->potential > 2) return fail(CT_E_CONFIG, "bad potential %d", r->potential);
+    if (r->potential < 0 || r->potential > 3) return fail(CT_E_CONFIG, "bad potential %d", r->potential);
+    if (r->curvature != CT_CURV_HUBER && r->curvature != CT_CURV_MAX) return fail(CT_E_CONFIG, "bad curvature");
+    if (r->potential == CT_POT_QGGMRF && !(r->q >= 1.0 && r->q <= 2.0))
+        return fail(CT_E_CONFIG, "q-GGMRF needs 1 <= q <= 2 (got %g)", r->q);
     if (!(r->delta > 0)) return fail(CT_E_CONFIG, "delta must be > 0");
     if (r->n_dirs != 4 && r->n_dirs != 13) return fail(CT_E_CONFIG, "n_dirs must be 4 or 13");
     if (g->G.dim == 2 && r->n_dirs != 4) return fail(CT_E_CONFIG, "2-D geometry uses n_dirs = 4");
@@ -294,6 +297,12 @@ static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp)
     rp.inv_delta = (float)(1.0 / r->delta);
     rp.potential = r->potential;
     rp.n_dirs = r->n_dirs;
+    rp.maxcurv = r->curvature == CT_CURV_MAX;
+    double bs = 0.0;
+    for (int i = 0; i < r->n_dirs; i++) bs += 2.0 * r->beta[i];
+    rp.bsum = (float)bs;
+    rp.q = (float)(r->potential == CT_POT_QGGMRF ? r->q : 2.0);
+    rp.qexp = 2.f - rp.q;
     return CT_OK;
 }
 
@@ -482,7 +491,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                     (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf,
                     (uintptr_t)xt};
         key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi, (double)p->variant,
-                    (double)rp.potential, (double)rp.delta, (double)rp.n_dirs};
+                    (double)rp.potential, (double)rp.delta, (double)rp.n_dirs, (double)rp.maxcurv, (double)rp.q};
         for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
         std::lock_guard<std::mutex> lk(const_cast<ct_geom*>(g)->mu);
         auto it = g->graphs.find(key);

@@ -11,6 +11,9 @@ struct RegParams {
     float beta[13];
     float delta, inv_delta;
     int potential, n_dirs;
+    int maxcurv;          // D_R with omega(0) = 1 (CT_CURV_MAX)
+    float bsum;           // sum_d 2 beta_d: the interior maximum-curvature sum
+    float q, qexp;        // q-GGMRF exponent q and 2 - q
 };
 
 // x_pair: (xa, xb); with ctl != nullptr the forward reads the buffer written

@@ -37,10 +37,14 @@ static_assert(dir_x(6) == -1 && dir_y(8) == -1 && dir_z(4) == 1 && dir_x(4) == 0
 // Potential in scaled form: tp = t / delta.  Returns omega(t) = phi'(t)/t and
 // tp * omega; phi'(t) = delta * tp * omega for all three potentials.
 template <int POT>
-__device__ __forceinline__ float omega_scaled(float tp) {
+__device__ __forceinline__ float omega_scaled(float tp, const RegParams& rp) {
     if (POT == 0) return 1.f;                                   // quadratic
     if (POT == 1) return rsqrt_ftz(fmaf(tp, tp, 1.f));          // hyperbola
-    return __fdividef(1.f, 1.f + fabsf(tp));                    // Fair
+    if (POT == 2) return __fdividef(1.f, 1.f + fabsf(tp));      // Fair
+    // q-GGMRF (p = 2): u = |t/delta|^(2-q), omega = (2 + q u) / (2 (1 + u)^2)
+    const float u = exp2f(rp.qexp * __log2f(fmaxf(fabsf(tp), 1e-30f)));   // 0^0 = 1 when q = 2
+    const float v = 1.f + u;
+    return __fdividef(fmaf(rp.q, u, 2.f), 2.f * v * v);
 }
 
 // 26/8-neighbour sums over a register window W[slot][dy+1][dx+1] of x/delta
@@ -56,7 +60,7 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
                                                bool kp, float& gs_out, float& cs_out) {
     const float xv = W[ZB][1][1];
     const float kj = KAPPA ? K[ZB][1][1] : 1.f;
-    float gs = 0.f, cs = 0.f;
+    float gs = 0.f, cs = 0.f, cmax = 0.f;
 #pragma unroll
     for (int d = 0; d < NDIRS; d++) {
         const int ox = dir_x(d), oy = dir_y(d), oz = dir_z(d);
@@ -64,7 +68,7 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
         if (!CHECK && !KAPPA) {
             const float tp = xv - W[zp][1 + oy][1 + ox];
             const float tm = xv - W[zm][1 - oy][1 - ox];
-            const float op = omega_scaled<POT>(tp), om = omega_scaled<POT>(tm);
+            const float op = omega_scaled<POT>(tp, rp), om = omega_scaled<POT>(tm, rp);
             gs = fmaf(rp.beta[d], fmaf(tp, op, tm * om), gs);
             cs = fmaf(rp.beta[d], op + om, cs);
         } else {
@@ -78,15 +82,17 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
                 if (ok) {
                     const float wgt = KAPPA ? rp.beta[d] * kj * K[zs][1 + sy][1 + sx] : rp.beta[d];
                     const float t = xv - W[zs][1 + sy][1 + sx];
-                    const float o = omega_scaled<POT>(t);
+                    const float o = omega_scaled<POT>(t, rp);
                     gs = fmaf(wgt, t * o, gs);
                     cs = fmaf(wgt, o, cs);
+                    cmax += wgt;
                 }
             }
         }
     }
     gs_out = gs;
-    cs_out = cs;
+    // maximum curvature: omega(0) = 1 for every in-volume neighbour (interior, no kappa: bsum)
+    cs_out = rp.maxcurv ? ((!CHECK && !KAPPA) ? rp.bsum : cmax) : cs;
 }
 
 // Arguments of the update-family kernels (k_update, k_update_pre).
@@ -378,7 +384,8 @@ static void upd_select(const DGeom& G, const RegParams& rp, const Ctl* ctl, cons
     switch (rp.potential) {
         case 0: CTR_UPD_CASE(0) break;
         case 1: CTR_UPD_CASE(1) break;
-        default: CTR_UPD_CASE(2) break;
+        case 2: CTR_UPD_CASE(2) break;
+        default: CTR_UPD_CASE(3) break;
     }
 #undef CTR_UPD_CASE
 }

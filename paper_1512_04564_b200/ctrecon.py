@@ -19,7 +19,8 @@ CT_OK, CT_E_SHAPE, CT_E_CONFIG, CT_E_NUMERIC, CT_E_DIVERGED, CT_E_CUDA, CT_E_NCC
 STATUS_NAMES = ["CT_OK", "CT_E_SHAPE", "CT_E_CONFIG", "CT_E_NUMERIC", "CT_E_DIVERGED", "CT_E_CUDA",
                 "CT_E_NCCL", "CT_E_NOMEM"]
 CT_DET_FLAT, CT_DET_ARC = 0, 1
-CT_POT = {"quadratic": 0, "hyperbola": 1, "fair": 2}
+CT_POT = {"quadratic": 0, "hyperbola": 1, "fair": 2, "qggmrf": 3}
+CT_CURV = {"huber": 0, "max": 1}
 RHO_CONTINUATION, RHO_FIXED = 0, 1
 PROPOSED, SIMPLE = 0, 1   # oslalm_variant: Algorithm 1 / Algorithm 2
 INIT_LAST_SUBSET, INIT_FULL = 0, 1
@@ -50,7 +51,7 @@ class ct_views(ctypes.Structure):
 
 class ct_reg_desc(ctypes.Structure):
     _fields_ = [("potential", ctypes.c_int32), ("delta", ctypes.c_double), ("n_dirs", ctypes.c_int32),
-                ("beta", ctypes.c_double * 13)]
+                ("beta", ctypes.c_double * 13), ("curvature", ctypes.c_int32), ("q", ctypes.c_double)]
 
 
 class oslalm_params(ctypes.Structure):
@@ -144,10 +145,12 @@ def geom_desc(g):
                         g["source_z0"])
 
 
-def reg_desc(potential, delta, betas, n_dirs):
+def reg_desc(potential, delta, betas, n_dirs, curvature="huber", q=1.2):
     r = ct_reg_desc()
     r.potential = CT_POT[potential]
     r.delta = float(delta)
+    r.curvature = CT_CURV[curvature]
+    r.q = float(q)
     r.n_dirs = int(n_dirs)
     for i in range(13):
         r.beta[i] = float(betas[i]) if i < len(betas) else 0.0

@@ -31,7 +31,8 @@ class Recon:
         self.x = torch.as_tensor(x0).to(**f32).contiguous().clone()
         self.g = torch.zeros_like(self.x)
         self.htilde = torch.zeros_like(self.x)
-        self.reg = C.reg_desc(reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"])
+        self.reg = C.reg_desc(reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"],
+                              reg.get("curvature", "huber"), reg.get("q", 1.2))
         self.params = C.params(solver["M"], solver["alpha"],
                                C.RHO_FIXED if solver.get("rho_mode") == "fixed" else C.RHO_CONTINUATION,
                                solver.get("rho_fixed", 0.0),

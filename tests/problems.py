@@ -65,4 +65,5 @@ def config_problem(name, device="cpu", **shrink):
 
 def oracle_problem(pb):
     r = pb["reg"]
-    return alg.Problem(pb["geom"], pb["y"], pb["w"], r["potential"], r["delta"], r["betas"], r["n_dirs"])
+    return alg.Problem(pb["geom"], pb["y"], pb["w"], r["potential"], r["delta"], r["betas"], r["n_dirs"],
+                       q=r.get("q", 1.2), curvature=r.get("curvature", "huber"))

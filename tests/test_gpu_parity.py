@@ -101,22 +101,24 @@ def test_sqs_diag_parity(C, name):
         C.ct_geom_destroy(h)
 
 
-@pytest.mark.parametrize("pot", ["hyperbola", "fair", "quadratic"])
+@pytest.mark.parametrize("pot", ["hyperbola", "fair", "quadratic", "qggmrf"])
 @pytest.mark.parametrize("kind", ["fan2d_arc", "helical_arc"])
 @pytest.mark.parametrize("use_kappa", [False, True])
-def test_reg_grad_parity(C, pot, kind, use_kappa):
+@pytest.mark.parametrize("curvature", ["huber", "max"])
+def test_reg_grad_parity(C, pot, kind, use_kappa, curvature):
     g = tiny(kind, nx=37, ny=21, nz=9) if kind == "helical_arc" else tiny(kind, nx=37, ny=21)
     rng = np.random.default_rng(9)
     x = 0.02 * rng.random(P.vol_shape(g))
     kap = rng.uniform(0.5, 1.5, x.shape) if use_kappa else None
     nd = 13 if g["dim"] == 3 else 4
     betas = list(rng.uniform(0.5, 2.0, nd))
-    _, gr, cv = P.reg(g, pot, 0.01, betas, nd, x, kap)
+    _, gr, cv = P.reg(g, pot, 0.01, betas, nd, x, kap, q=1.3, curvature=curvature)
     h = C.ct_geom_create(C.geom_desc(g))
     try:
         gd = torch.empty(x.shape, dtype=torch.float32, device="cuda")
         cd = torch.empty_like(gd)
-        C.ct_reg_grad(h, C.reg_desc(pot, 0.01, betas, nd), dev(x), gd, cd, kappa=dev(kap) if use_kappa else None)
+        C.ct_reg_grad(h, C.reg_desc(pot, 0.01, betas, nd, curvature, 1.3), dev(x), gd, cd,
+                      kappa=dev(kap) if use_kappa else None)
         assert rel(host(gd), gr) <= 1e-5
         assert rel(host(cd), cv) <= 1e-5
     finally:
@@ -187,6 +189,21 @@ def test_alpha1_alg1_equals_alg2_on_gpu(C):
         rec.close()
     assert rel(outs[1][0], outs[0][0]) <= 1e-5
     assert rel(outs[1][1], outs[0][1]) <= 1e-5
+
+
+@pytest.mark.parametrize("kind", ["helical_arc", "fan2d_arc"])
+def test_qggmrf_max_curvature_solve_matches_oracle(C, kind):
+    """q-GGMRF potential with the maximum-curvature D_R
+    through the solver against the oracle's Algorithm 1."""
+    pb = synthetic_problem(tiny(kind), M=3)
+    pb["reg"] = dict(pb["reg"], potential="qggmrf", q=1.2, curvature="max")
+    prob = oracle_problem(pb)
+    xo, go, ho = alg.alg1(prob, pb["x0"], 3, 1.999, 2, DL=pb["DL"])
+    rec = _gpu_recon(pb, dl=pb["DL"])
+    rec.run(6)
+    assert rel(host(rec.x), xo) <= 1e-4
+    assert rel(host(rec.g), go) <= 1e-3
+    rec.close()
 
 
 def test_c1_full_solve_matches_oracle(C):

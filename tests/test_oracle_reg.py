@@ -8,7 +8,7 @@ import pytest
 from oracle import projector as P
 from synth.configs import DIRECTIONS, _geom
 
-POTS = ["hyperbola", "fair", "quadratic"]
+POTS = ["hyperbola", "fair", "quadratic", "qggmrf"]
 
 
 def vol(nx, ny, nz, dz=1.0):
@@ -85,8 +85,18 @@ def test_two_voxel_hand_expansion(pot):
     elif pot == "hyperbola":
         q = math.sqrt(1 + (t / d) ** 2)
         phi, dphi, om = d * d * (q - 1), t / q, 1 / q
-    else:
+    elif pot == "fair":
         phi, dphi, om = d * d * (abs(t) / d - math.log(1 + abs(t) / d)), t / (1 + abs(t) / d), 1 / (1 + abs(t) / d)
+    else:   # q-GGMRF, p = 2, q = 1.2 (the default): phi = (t^2/2)/(1 + |t/d|^0.8)
+        u = (abs(t) / d) ** 0.8
+        phi = 0.5 * t * t / (1 + u)
+        h = 1e-6       # phi' by a central difference of phi, omega = phi'/t
+        dphi = (0.5 * (t + h) ** 2 / (1 + (abs(t + h) / d) ** 0.8) - 0.5 * (t - h) ** 2 / (1 + (abs(t - h) / d) ** 0.8)) / (2 * h)
+        om = dphi / t
+        assert np.isclose(R, beta * phi, rtol=1e-14)
+        assert np.allclose(gr.ravel(), [beta * dphi, -beta * dphi], rtol=1e-8)
+        assert np.allclose(cv.ravel(), [2 * beta * om] * 2, rtol=1e-8)
+        return
     assert np.isclose(R, beta * phi, rtol=1e-14)
     assert np.allclose(gr.ravel(), [beta * dphi, -beta * dphi], rtol=1e-14)
     assert np.allclose(cv.ravel(), [2 * beta * om] * 2, rtol=1e-14)
@@ -129,3 +139,46 @@ def test_sampled_reg_matches_full():
     idx = rng.integers(0, x.size, 40)
     g2, c2 = P.reg_at(g, "hyperbola", 0.05, np.arange(1, 14) / 7.0, 13, x, idx, kap)
     assert np.allclose(g2, gr.ravel()[idx], rtol=1e-15) and np.allclose(c2, cv.ravel()[idx], rtol=1e-15)
+
+
+def test_qggmrf_special_values():
+    # p = 2 q-GGMRF (Thibault et al. 2007; PAPER.md:467 chest data):
+    #   q = 2 reduces to the quadratic t^2/4 (u = 1 for every t);
+    #   at t = delta (u = 1): phi = delta^2/4, phi' = delta (2 + q)/8, omega = (2 + q)/8;
+    #   omega(0) = 1 like the other potentials (max curvature = 2 sum beta).
+    g = vol(2, 1, 1)
+    rng = np.random.default_rng(3)
+    for t in rng.uniform(-3, 3, 5):
+        R, gr, cv = P.reg(g, "qggmrf", 0.7, [1.0], 1, np.array([[[t, 0.0]]]), q=2.0)
+        assert np.isclose(R, t * t / 4, rtol=1e-14) and np.isclose(gr.ravel()[0], t / 2, rtol=1e-14)
+        assert np.isclose(cv.ravel()[0], 1.0, rtol=1e-14)
+    d, q = 0.3, 1.3
+    R, gr, cv = P.reg(g, "qggmrf", d, [1.0], 1, np.array([[[d, 0.0]]]), q=q)
+    assert np.isclose(R, d * d / 4, rtol=1e-14)
+    assert np.isclose(gr.ravel()[0], d * (2 + q) / 8, rtol=1e-14)
+    assert np.isclose(cv.ravel()[0], 2 * (2 + q) / 8, rtol=1e-14)
+    _, _, c0 = P.reg(g, "qggmrf", d, [1.0], 1, np.zeros((1, 1, 2)), q=q)
+    assert np.allclose(c0, 2.0)
+
+
+@pytest.mark.parametrize("pot", POTS)
+def test_max_curvature_majorizes(pot):
+    # curvature="max": D_R = 2 sum_n beta kappa kappa omega(0) = 2 sum beta kappa kappa, independent of x;
+    # it is >= the Huber curvature (omega is largest at 0 for these potentials) and the SQS
+    # inequality R(z) <= R(x) + <grad, z - x> + |z - x|^2_{D_R} / 2 still holds.
+    g = vol(5, 4, 3)
+    rng = np.random.default_rng(21)
+    x = rng.random((3, 4, 5)) * 0.1
+    kap = rng.uniform(0.5, 1.5, x.shape)
+    betas = rng.uniform(0.5, 2.0, 13)
+    R0, gr, ch = P.reg(g, pot, 0.05, betas, 13, x, kap)
+    _, gm, cm = P.reg(g, pot, 0.05, betas, 13, x, kap, curvature="max")
+    _, _, cq = P.reg(g, "quadratic", 0.05, betas, 13, rng.random(x.shape), kap)
+    assert np.allclose(gm, gr, rtol=1e-15)
+    assert np.allclose(cm, cq, rtol=1e-14)          # = the quadratic potential's (omega = 1) curvature
+    assert np.all(cm >= ch * (1 - 1e-14))
+    for _ in range(5):
+        z = x + 0.05 * rng.standard_normal(x.shape)
+        Rz = P.reg(g, pot, 0.05, betas, 13, z, kap)[0]
+        Q = R0 + np.sum(gr * (z - x)) + 0.5 * np.sum(cm * (z - x) ** 2)
+        assert Rz <= Q + 1e-12 * max(1.0, abs(Q))
