@@ -181,6 +181,16 @@ ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, 
 ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist* dist, float* d_out, void* workspace,
                       size_t workspace_bytes, ct_stream s);
 
+/* Resolution-uniformity weights of the regulariser (kappa_n, cited
+ * to [fessler:96:srp]; the formula is SPEC.md:529-531's reading):
+ *   kappa_j = sqrt([A'W1]_j / [A'1]_j),  0/0 = 1,
+ * over all views, A' the exact transpose of ct_forward (L_z included).
+ * w: full sinogram weights float[na][nt][ns] (NULL = all ones -> kappa = 1).
+ * kappa_out: volume.  workspace: >= (nvox + nt*ns) * 4 bytes (more = fewer
+ * chunks).  Errors: CT_E_CONFIG (NULL), CT_E_NOMEM, CT_E_CUDA. */
+ct_status ct_kappa_weights(const ct_geom* g, const float* w, float* kappa_out, void* workspace,
+                           size_t workspace_bytes, ct_stream s);
+
 /* grad = nabla R(x), curv = Huber curvature D_R(x) = 2 sum beta kappa kappa omega(x_j - x_n)
  * (factor 2 = separable quadratic surrogate split, R6).
  * kappa NULL = ones; curv NULL = skip. */

@@ -87,6 +87,18 @@ class Problem:
         return 0.5 * float(np.sum(self.w * r * r)) + self.reg_value(x)
 
 
+def kappa_weights(g, w):
+    """Resolution-uniformity weights kappa of Eq. 35 (PAPER.md:319-321 cites them;
+    formula as SPEC.md:529-531 reads [fessler:96:srp]):
+    kappa_j = sqrt([A'W1]_j / [A'1]_j), 0/0 = 1, over all views."""
+    aw = P.back(g, np.asarray(w, dtype=np.float64))
+    a1 = P.back(g, np.ones(P.proj_shape(g, g["na"])))
+    out = np.ones_like(a1)
+    pos = a1 > 0
+    out[pos] = np.sqrt(aw[pos] / a1[pos])
+    return out
+
+
 def _x_update(x, s, gradR, denom):
     """x+ = [x - (rho D_L + D_R)^{-1}(s + grad R(x))]_Omega; zero denominator keeps x."""
     safe = np.where(denom > 0, denom, 1.0)

@@ -94,6 +94,8 @@ static ct_status check_async() {
     return CT_OK;
 }
 
+static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
 // ------------------------------------------------------------------ geometry
 static ct_status validate_desc(const ct_geom_desc* d) {
     if (!d) return fail(CT_E_CONFIG, "ct_geom_desc is NULL");
@@ -280,6 +282,34 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
     return CT_OK;
 }
 
+extern "C" ct_status ct_kappa_weights(const ct_geom* g, const float* w, float* kappa_out, void* workspace,
+                                      size_t workspace_bytes, ct_stream s) {
+    if (!g || !kappa_out || !workspace) return fail(CT_E_CONFIG, "ct_kappa_weights: NULL argument");
+    const size_t vol = align_up(sizeof(float) * (size_t)g->G.nvox);
+    const size_t per_view = (size_t)g->G.nt * g->G.ns * sizeof(float);
+    if (workspace_bytes < vol + per_view)
+        return fail(CT_E_NOMEM, "ct_kappa_weights: workspace %zu < %zu bytes", workspace_bytes, vol + per_view);
+    DeviceGuard guard(g->device);
+    cudaStream_t cs = (cudaStream_t)s;
+    float* aone = (float*)workspace;                      // A'1
+    float* ones = (float*)((char*)workspace + vol);       // a chunk of all-ones views
+    const int chunk = (int)std::min<size_t>((workspace_bytes - vol) / per_view, 65535);
+    const long long nproj = (long long)chunk * g->G.nt * g->G.ns;
+    launch_fill(ones, nproj, 1.f, cs);
+    CT_CUDA(cudaMemsetAsync(aone, 0, sizeof(float) * g->G.nvox, cs));
+    CT_CUDA(cudaMemsetAsync(kappa_out, 0, sizeof(float) * g->G.nvox, cs));
+    const size_t view_elems = (size_t)g->G.nt * g->G.ns;
+    for (int c0 = 0; c0 < g->d.na; c0 += chunk) {
+        const int cnt = std::min(chunk, g->d.na - c0);
+        Views vv{c0, 1, cnt};
+        launch_back(g->G, g->vtab, nullptr, vv, ones, 1.0f, BK_ACCUM, g->G.dim == 3, aone, nullptr, nullptr, cs);
+        launch_back(g->G, g->vtab, nullptr, vv, w ? w + (size_t)c0 * view_elems : ones, 1.0f, BK_ACCUM,
+                    g->G.dim == 3, kappa_out, nullptr, nullptr, cs);     // A'W1 (W1 = w)
+    }
+    launch_kappa_ratio(g->G.nvox, kappa_out, aone, kappa_out, cs);
+    return check_async();
+}
+
 static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp) {
     if (!r) return fail(CT_E_CONFIG, "ct_reg_desc is NULL");
     if (r->potential < 0 || r->potential > 3) return fail(CT_E_CONFIG, "bad potential %d", r->potential);
@@ -322,7 +352,6 @@ struct WsLayout {
     size_t ctl, xalt, xt, r, zeta, gradr, curvr, flag, dsum, total;
 };
 
-static size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
 static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dist* dist) {
     const int world = dist ? dist->world : 1;

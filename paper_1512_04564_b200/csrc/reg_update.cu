@@ -465,6 +465,21 @@ __global__ void k_init_from_zeta(long long n, const float* __restrict__ zeta, fl
 
 __global__ void k_advance(Ctl* ctl) { ctl->k += 1; }
 
+__global__ void k_fill(float* p, long long n, float v) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x)
+        p[idx] = v;
+}
+
+// kappa_j = sqrt([A'W1]_j / [A'1]_j), 0/0 = 1
+__global__ void k_kappa_ratio(long long n, const float* __restrict__ a, const float* __restrict__ b, float* kappa) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const float bv = b[idx];
+        kappa[idx] = bv > 0.f ? sqrtf(a[idx] / bv) : 1.f;
+    }
+}
+
 __global__ void k_state_h(long long n, const float* __restrict__ dl, const float* __restrict__ x,
                           const float* __restrict__ ht, float* h) {
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -507,6 +522,14 @@ void launch_gh_update(const DGeom& G, const Ctl* ctl, const float* zeta, float* 
 }
 void launch_init_from_zeta(const DGeom& G, const float* zeta, float* g, float* ht, cudaStream_t s) {
     k_init_from_zeta<<<grid_for(G.nvox), 256, 0, s>>>(G.nvox, zeta, g, ht);
+    launches_add(1);
+}
+void launch_fill(float* p, long long n, float v, cudaStream_t s) {
+    k_fill<<<grid_for(n), 256, 0, s>>>(p, n, v);
+    launches_add(1);
+}
+void launch_kappa_ratio(long long n, const float* a, const float* b, float* kappa, cudaStream_t s) {
+    k_kappa_ratio<<<grid_for(n), 256, 0, s>>>(n, a, b, kappa);
     launches_add(1);
 }
 void launch_advance(Ctl* ctl, cudaStream_t s) {

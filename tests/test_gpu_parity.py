@@ -206,6 +206,34 @@ def test_qggmrf_max_curvature_solve_matches_oracle(C, kind):
     rec.close()
 
 
+@pytest.mark.parametrize("name", KINDS)
+def test_kappa_weights_parity_and_kappa_solve(C, name):
+    """ct_kappa_weights (SPEC.md:529-531 reading of P:321's kappa) against the oracle,
+    with a workspace that forces chunking; then Algorithm 1 with that kappa."""
+    g = geom_of(name)
+    pb = synthetic_problem(g, M=3)
+    ko = alg.kappa_weights(g, pb["w"])
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        kd = torch.empty(P.vol_shape(g), dtype=torch.float32, device="cuda")
+        nvox = int(np.prod(P.vol_shape(g)))
+        per_view = g["ns"] * (g["nt"] if g["dim"] == 3 else 1) * 4
+        ws = torch.empty(((nvox * 4 + 255) // 256) * 256 + 3 * per_view + 5, dtype=torch.uint8, device="cuda")
+        C.ct_kappa_weights(h, dev(pb["w"]), kd, ws)
+        assert rel(host(kd), ko) <= 1e-5
+    finally:
+        C.ct_geom_destroy(h)
+    prob = oracle_problem(pb)
+    prob.kappa = ko
+    xo = alg.alg1(prob, pb["x0"], 3, 1.999, 2, DL=pb["DL"])[0]
+    from paper_1512_04564_b200.recon import Recon
+    rec = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], kappa=host(kd))
+    rec.set_DL(pb["DL"])
+    rec.run(6)
+    assert rel(host(rec.x), xo) <= 1e-4
+    rec.close()
+
+
 def test_c1_full_solve_matches_oracle(C):
     """BASELINE configs[0]: 128^2 fan, 180 views, M = 4, 20 iterations, alpha = 1.999."""
     pb = config_problem("c1")

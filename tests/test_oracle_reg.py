@@ -182,3 +182,20 @@ def test_max_curvature_majorizes(pot):
         Rz = P.reg(g, pot, 0.05, betas, 13, z, kap)[0]
         Q = R0 + np.sum(gr * (z - x)) + 0.5 * np.sum(cm * (z - x) ** 2)
         assert Rz <= Q + 1e-12 * max(1.0, abs(Q))
+
+
+def test_kappa_weights_closed_forms():
+    # W = I gives kappa = 1; W = c I gives kappa = sqrt(c) (constant factors
+    # cancel); voxels no ray reaches (0/0) get 1.  A voxel-dependent W changes kappa.
+    from oracle import alg
+    from tests.geoms import tiny
+    g = tiny("helical_arc")
+    shp = P.proj_shape(g, g["na"])
+    k1 = alg.kappa_weights(g, np.ones(shp))
+    assert np.allclose(k1, 1.0, rtol=1e-13)
+    kc = alg.kappa_weights(g, 2.5 * np.ones(shp))
+    assert np.allclose(kc, math.sqrt(2.5), rtol=1e-13)
+    w = np.random.default_rng(4).uniform(0.5, 2.0, shp)
+    kw = alg.kappa_weights(g, w)
+    assert np.all(kw > math.sqrt(0.5) - 1e-12) and np.all(kw < math.sqrt(2.0) + 1e-12)
+    assert np.std(kw) > 1e-3
