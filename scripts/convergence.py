@@ -38,8 +38,11 @@ def main():
 
     def recon(**solver):
         s = dict(base)
+        reg = dict(inp["reg"])
+        reg.update(solver.pop("reg", {}))
+        solver.pop("dl_scale", None)
         s.update(solver)
-        r = Recon(g, inp["reg"], s, inp["y"], inp["w"], inp["x0"])
+        r = Recon(g, reg, s, inp["y"], inp["w"], inp["x0"])
         return r
 
     # reference: Alg. 1, M = 1, alpha = 1.999, until converged
@@ -63,13 +66,16 @@ def main():
         "unrelaxed_M": dict(M=M, alpha=1.0),
         "unrelaxed_2M": dict(M=2 * M, alpha=1.0),
         "os_sqs_M": dict(M=M, alpha=1.0, variant="simple", rho_mode="fixed", rho_fixed=1.0),
+        # supplement P:1272: majorization study (maximum vs Huber curvature; D_L scaled by 2)
+        "proposed_maxcurv": dict(M=M, alpha=1.999, reg=dict(curvature="max")),
+        "proposed_2DL": dict(M=M, alpha=1.999, dl_scale=2.0),
     }
     out = {"config": name, "M": M, "iters": iters, "ref": {"algorithm": "Alg. 1, M = 1, alpha = 1.999",
            "iters": ref_iters, "rel_move_per_100_iters": moves, "seconds": t_ref}, "rms": {}}
     x0_rms = float((inp["x0"].to(xref.device) - xref).pow(2).mean().sqrt())
     for key, sv in runs.items():
-        r = recon(**sv)
-        r.set_DL(dl)
+        r = recon(**dict(sv))
+        r.set_DL(dl * sv.get("dl_scale", 1.0))   # study harness: D_L majorizer scaled
         rms = [x0_rms]
         for it in range(iters):
             r.run(sv["M"])
@@ -79,9 +85,9 @@ def main():
     ref.close()
     hu = 1000.0 / 0.02
     lines = ["RMS(x_k - x*) in HU (mu_water = 0.02/mm), %s, M = %d" % (name, M),
-             "iter " + " ".join("%14s" % k for k in runs)]
+             "iter " + " ".join("%16s" % k for k in runs)]
     for it in list(range(0, min(iters, 10) + 1)) + list(range(15, iters + 1, 5)):
-        lines.append("%4d " % it + " ".join("%14.2f" % (out["rms"][k][it] * hu) for k in runs))
+        lines.append("%4d " % it + " ".join("%16.2f" % (out["rms"][k][it] * hu) for k in runs))
     print("\n".join(lines))
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "convergence_%s.json" % name), "w") as f:
