@@ -181,6 +181,18 @@ ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, 
 ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist* dist, float* d_out, void* workspace,
                       size_t workspace_bytes, ct_stream s);
 
+/* Initial image by filtered back-projection ("an initial (FBP)
+ * image"; the paper does not define it): textbook fan-beam FBP (equiangular
+ * arc / equispaced flat detector; Kak & Slaney ch. 3.4) for 2-D, Feldkamp
+ * (FDK) for axial cone scans; Ram-Lak filter, bilinear interpolation,
+ * full 360-degree orbit (oracle/fbp.py).
+ * proj: line integrals float[na][nt][ns] (all views); x_out: volume.
+ * workspace >= na*nt*ns*4 bytes (the filtered sinogram).
+ * Errors: CT_E_CONFIG (helical scan, orbit != 360 degrees, NULL,
+ * ns > 18000), CT_E_NOMEM, CT_E_CUDA. */
+ct_status ct_fbp(const ct_geom* g, const float* proj, float* x_out, void* workspace, size_t workspace_bytes,
+                 ct_stream s);
+
 /* Resolution-uniformity weights of the regulariser (kappa_n, cited
  * to [fessler:96:srp]; the formula is SPEC.md:529-531's reading):
  *   kappa_j = sqrt([A'W1]_j / [A'1]_j),  0/0 = 1,

@@ -282,6 +282,19 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
     return CT_OK;
 }
 
+extern "C" ct_status ct_fbp(const ct_geom* g, const float* proj, float* x_out, void* workspace,
+                            size_t workspace_bytes, ct_stream s) {
+    if (!g || !proj || !x_out || !workspace) return fail(CT_E_CONFIG, "ct_fbp: NULL argument");
+    if (std::fabs(g->d.orbit_deg - 360.0) > 1e-9) return fail(CT_E_CONFIG, "ct_fbp: needs a 360-degree orbit");
+    if (g->G.dim == 3 && g->d.pitch != 0.0) return fail(CT_E_CONFIG, "ct_fbp: helical scans are not supported");
+    if (g->d.ns > 18000) return fail(CT_E_CONFIG, "ct_fbp: ns > 18000");
+    const size_t need = sizeof(float) * (size_t)g->d.na * g->G.nt * g->G.ns;
+    if (workspace_bytes < need) return fail(CT_E_NOMEM, "ct_fbp: workspace %zu < %zu bytes", workspace_bytes, need);
+    DeviceGuard guard(g->device);
+    launch_fbp(g->G, g->vtab, proj, (float*)workspace, x_out, g->d.dsd, (cudaStream_t)s);
+    return check_async();
+}
+
 extern "C" ct_status ct_kappa_weights(const ct_geom* g, const float* w, float* kappa_out, void* workspace,
                                       size_t workspace_bytes, ct_stream s) {
     if (!g || !kappa_out || !workspace) return fail(CT_E_CONFIG, "ct_kappa_weights: NULL argument");

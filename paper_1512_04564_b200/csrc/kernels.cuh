@@ -46,6 +46,10 @@ void launch_update_pre(const DGeom& G, const Ctl* ctl, const float* xin, float* 
                        float* ht, const float* zeta, const float* grad, const float* curv, float box_lo,
                        float box_hi, float* pfx, cudaStream_t s);
 
+// FBP / FDK initialiser (fbp.cu): filtered sinogram into qbuf (na views), image into out
+void launch_fbp(const DGeom& G, const float4* vtab, const float* proj, float* qbuf, float* out, double dsd,
+                cudaStream_t s);
+
 // elementwise helpers of ct_kappa_weights: fill with a constant; kappa = sqrt(a / b), 0/0 = 1
 void launch_fill(float* p, long long n, float v, cudaStream_t s);
 void launch_kappa_ratio(long long n, const float* a, const float* b, float* kappa, cudaStream_t s);

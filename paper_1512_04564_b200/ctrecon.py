@@ -65,7 +65,7 @@ class oslalm_state(ctypes.Structure):
                 ("k", ctypes.c_int64)]
 
 
-EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs_diag", "ct_kappa_weights",
+EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs_diag", "ct_kappa_weights", "ct_fbp",
            "ct_reg_grad",
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
@@ -91,6 +91,7 @@ def load():
     L.ct_sqs_diag.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.ct_reg_grad.argtypes = [vp, P(ct_reg_desc), vp, vp, vp, vp, vp]
     L.ct_kappa_weights.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.ct_fbp.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.oslalm_workspace_size.argtypes = [vp, P(oslalm_params), vp, P(ctypes.c_size_t)]
     L.oslalm_relaxed_solve.argtypes = [vp, vp, vp, P(ct_reg_desc), vp, vp, P(oslalm_params), P(oslalm_state),
                                        ctypes.c_int, vp, P(ctypes.c_double), vp, vp, ctypes.c_size_t, vp]
@@ -107,7 +108,7 @@ def load():
     L.ct_dist_destroy.restype = None
     L.ct_launch_count.restype = ctypes.c_int64
     L.ct_last_error.restype = ctypes.c_char_p
-    for name in ("ct_geom_create", "ct_forward", "ct_back", "ct_sqs_diag", "ct_kappa_weights", "ct_reg_grad",
+    for name in ("ct_geom_create", "ct_forward", "ct_back", "ct_sqs_diag", "ct_kappa_weights", "ct_fbp", "ct_reg_grad",
                  "oslalm_workspace_size",
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz"):
@@ -192,6 +193,11 @@ def ct_back(geom, proj, v, x_out, scale=1.0, accumulate=False, stream=None):
 def ct_sqs_diag(geom, w, d_out, workspace, dist=None, stream=None):
     _check(load().ct_sqs_diag(geom, _ptr(w), dist, _ptr(d_out), ctypes.c_void_p(workspace.data_ptr()),
                               workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def ct_fbp(geom, proj, x_out, workspace, stream=None):
+    _check(load().ct_fbp(geom, _ptr(proj), _ptr(x_out), ctypes.c_void_p(workspace.data_ptr()),
+                         workspace.numel() * workspace.element_size(), _stream(stream)))
 
 
 def ct_kappa_weights(geom, w, kappa_out, workspace, stream=None):

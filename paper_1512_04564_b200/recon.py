@@ -50,6 +50,14 @@ class Recon:
         C.ct_sqs_diag(self.h, self.w, self.dl, self.ws, dist=self.dist, stream=self.stream)
         return self.dl
 
+    def init_fbp(self):
+        """x = FBP / FDK of y (ct_fbp; "an initial (FBP) image"): 2-D fan and
+        axial cone scans with a 360-degree orbit.  Resets the solver state (k = 0)."""
+        ws = torch.empty(self.y.numel() * 4, dtype=torch.uint8, device=self.dev)
+        C.ct_fbp(self.h, self.y, self.x, ws, stream=self.stream)
+        self.state.k = 0
+        return self.x
+
     def set_DL(self, dl):
         self.dl = torch.as_tensor(dl).to(dtype=torch.float32, device=self.dev).contiguous()
 

@@ -234,6 +234,38 @@ def test_kappa_weights_parity_and_kappa_solve(C, name):
     rec.close()
 
 
+@pytest.mark.parametrize("name", ["fan2d_arc", "fan2d_flat", "axial_flat", "axial_arc", "c1"])
+def test_fbp_parity(C, name):
+    """ct_fbp (FBP / FDK initialiser) against oracle/fbp.py on the
+    analytic line integrals of the config's random-ellipse phantom."""
+    from oracle import fbp as F
+    from synth.phantom import analytic_sinogram, sample_ellipsoids
+    g = tiny("axial_flat", det="arc", ds=0.018 * 180.0 / 1.0) if name == "axial_arc" else geom_of(name)
+    ells = sample_ellipsoids(g, 6, 11)
+    sino = analytic_sinogram(g, ells, sub_s=1, sub_t=1).numpy()
+    ref = F.fbp(g, sino)
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        out = torch.empty(P.vol_shape(g), dtype=torch.float32, device="cuda")
+        ws = torch.empty(sino.size * 4, dtype=torch.uint8, device="cuda")
+        C.ct_fbp(h, dev(sino), out, ws)
+        assert rel(host(out), ref) <= 1e-4, rel(host(out), ref)
+    finally:
+        C.ct_geom_destroy(h)
+
+
+def test_fbp_rejects_helical(C):
+    g = tiny("helical_arc")
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        out = torch.empty(P.vol_shape(g), dtype=torch.float32, device="cuda")
+        ws = torch.empty(g["na"] * g["nt"] * g["ns"] * 4, dtype=torch.uint8, device="cuda")
+        with pytest.raises(C.CtError):
+            C.ct_fbp(h, torch.zeros(P.proj_shape(g, g["na"]), device="cuda"), out, ws)
+    finally:
+        C.ct_geom_destroy(h)
+
+
 def test_c1_full_solve_matches_oracle(C):
     """BASELINE configs[0]: 128^2 fan, 180 views, M = 4, 20 iterations, alpha = 1.999."""
     pb = config_problem("c1")
