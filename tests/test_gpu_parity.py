@@ -367,7 +367,7 @@ def test_deterministic_repeat(C):
     assert np.array_equal(outs[0], outs[1])
 
 
-@pytest.mark.parametrize("name", ["c4", "c3", "c2"])
+@pytest.mark.parametrize("name", ["c5", "c4", "c3", "c2"])
 def test_full_size_subiteration_sampled(C, name):
     """BASELINE config at full size, bench launch configuration (graph-replayed
     solve): one sub-iteration from a seeded state (k = 5, so subset 5 and
