@@ -241,6 +241,35 @@ ct_status oslalm_relaxed_solve(const ct_geom* g, const float* y, const float* w,
                                int n_subiters, const float* x_ref, double* rms_per_iter, const ct_dist* dist,
                                void* workspace, size_t workspace_bytes, ct_stream s);
 
+/*
+ * Volume-domain (z-slab) decomposition:
+ * rank p of `world` owns the planes [z0, z0 + nz) given by ct_zslab_range
+ * (floor(p NZ / world) .. floor((p+1) NZ / world)) of x, g, htilde and D_L
+ * (arrays of nz * ny * nx floats, boundary layout); every rank holds the full
+ * y and w.  Per sub-iteration: slab x-update with one halo plane from each
+ * neighbour, halo exchange (ncclSend/Recv), forward projection of the slab
+ * for the subset's views, sum of the partial projections (ncclAllReduce of
+ * V_m nt ns floats instead of the view decomposition's NX NY NZ) and the
+ * weighted residual, back-projection onto the slab with the g / htilde
+ * epilogue: every volume kernel works on 1/world of the volume.
+ * One process per GPU: dist != NULL, nlocal = 1, the arrays of this rank.
+ * One process driving all slabs on one device: dist == NULL, nlocal = world,
+ * arrays indexed by rank (this is how the decomposition is tested on one GPU).
+ * kappa is not supported (ones).  workspace[i]: >= the bytes of
+ * oslalm_zslab_workspace_size for that slab, one buffer per local slab; slab
+ * 0's buffer also holds the shared residual.  The state's k must agree across
+ * slabs; k == 0 runs line 1 of Algorithm 1.  Errors as oslalm_relaxed_solve.
+ */
+ct_status ct_zslab_range(const ct_geom* g, int rank, int world, int* z0, int* nz);
+ct_status oslalm_zslab_workspace_size(const ct_geom* g, const oslalm_params* p, int rank, int world, size_t* bytes);
+/* D_L = diag(A'WA1) of the local slabs (same partial-projection sum). */
+ct_status ct_sqs_diag_zslab(const ct_geom* g, const float* w, int nlocal, int world, const ct_dist* dist,
+                            float* const* d_out, void* const* workspace, size_t workspace_bytes, ct_stream s);
+ct_status oslalm_zslab_solve(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
+                             const float* const* d_l, const oslalm_params* p, oslalm_state* st, int nlocal, int world,
+                             int n_subiters, const ct_dist* dist, void* const* workspace, size_t workspace_bytes,
+                             ct_stream s);
+
 /* Same as oslalm_relaxed_solve (no x_ref/rms) but runs the sub-iterations
  * eagerly with CUDA events around each kernel and returns, in host
  * kernel_ms[4], the summed device time of (0) stencil + x-update, (1)

@@ -691,6 +691,26 @@ extern "C" ct_status ct_sync(ct_stream s) {
 }
 
 // ------------------------------------------------------------------ NCCL
+// ------------------------------------------------------------------ accessors for zslab.cu
+ct_status ctr_fail(ct_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+const DGeom& ctr_geom_dev(const ct_geom* g) { return g->G; }
+const float4* ctr_geom_vtab(const ct_geom* g) { return g->vtab; }
+const ct_geom_desc& ctr_geom_desc(const ct_geom* g) { return g->d; }
+int ctr_geom_device(const ct_geom* g) { return g->device; }
+ncclComm_t ctr_dist_comm(const ct_dist* d) { return d->comm; }
+int ctr_dist_rank(const ct_dist* d) { return d->rank; }
+int ctr_dist_world(const ct_dist* d) { return d->world; }
+ct_status ctr_make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp) { return make_reg(g, r, rp); }
+ct_status ctr_validate_params(const ct_geom* g, const oslalm_params* p) { return validate_params(g, p); }
+
 extern "C" ct_status ct_nccl_unique_id(unsigned char id[128]) {
     if (!id) return fail(CT_E_CONFIG, "id is NULL");
     ncclUniqueId u;

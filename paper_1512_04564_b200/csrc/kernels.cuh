@@ -39,6 +39,12 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
                    const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s);
 
+// z-slab decomposition: the update with one halo plane of x below / above the slab
+// (x buffers xa, xb point at plane 0 of (nz + 2)-plane allocations)
+void launch_update_halo(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
+                        float* g, float* ht, float box_lo, float box_hi, float* pfx, bool halo_lo, bool halo_hi,
+                        cudaStream_t s);
+
 // multi-GPU path: fold the all-reduced zeta of the previous sub-iteration into
 // g, htilde (lines 7-8) and run lines 4-5 from precomputed grad R / D_R
 // (launch_reg on the new x); Ctl.k is one behind (the advance follows)

@@ -112,6 +112,7 @@ struct UpdArgs {
     float* pfx;           // z-prefix of x+ for the 3-D forward (NULL = none)
     float box_lo, box_hi;
     int CZ;               // voxels per z-chunk
+    int halo_lo, halo_hi; // z-slab decomposition: planes -1 / nz of x exist (neighbour slabs' halos)
 };
 
 enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
@@ -187,12 +188,13 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     // raw loads into a ring slot; the slot is scaled by 1/delta one step later.
     // Interior columns load the 3x3 block unconditionally from a clamped plane (a
     // plane outside the volume is never weighted: the stencil checks km/kp there).
+    const int klo = A.halo_lo ? -1 : 0, khi = A.halo_hi ? G.nz : G.nz - 1;   // readable planes of x
     auto load_plane = [&](auto slot_c, int k) {
         constexpr int S = decltype(slot_c)::value;
         if (inxy) {
-            const int kc = min(max(k, 0), G.nz - 1);
-            const float* __restrict__ p = x + ((unsigned)kc * nxy + col - nx - 1u);
-            const float* __restrict__ pk = KAPPA ? kappa + ((unsigned)kc * nxy + col - nx - 1u) : nullptr;
+            const int kc = min(max(k, klo), khi);
+            const float* __restrict__ p = x + ((long long)kc * nxy + col - nx - 1u);
+            const float* __restrict__ pk = KAPPA ? kappa + ((long long)kc * nxy + col - nx - 1u) : nullptr;
 #pragma unroll
             for (int dy = 0; dy < 3; dy++) {
 #pragma unroll
@@ -204,17 +206,17 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
                 if (KAPPA) pk += nx;
             }
         } else {
-            const bool ok = act && k >= 0 && k < G.nz;
-            const unsigned o = ok ? (unsigned)k * nxy + col : 0u;
+            const bool ok = act && k >= klo && k <= khi;
+            const long long o = ok ? (long long)k * nxy + col : 0;
 #pragma unroll
             for (int dy = -1; dy <= 1; dy++) {
                 const bool vy = dy < 0 ? jm : (dy > 0 ? jp : true);
-                const unsigned ro = o + (unsigned)(dy * (int)nx);
+                const long long ro = o + (long long)dy * (int)nx;
 #pragma unroll
                 for (int dx = -1; dx <= 1; dx++) {
                     const bool v = ok && vy && (dx < 0 ? im : (dx > 0 ? ip : true));
-                    W[S][dy + 1][dx + 1] = v ? __ldg(x + (ro + (unsigned)dx)) : 0.f;
-                    if (KAPPA) K[S][dy + 1][dx + 1] = v ? __ldg(kappa + (ro + (unsigned)dx)) : 0.f;
+                    W[S][dy + 1][dx + 1] = v ? __ldg(x + (ro + dx)) : 0.f;
+                    if (KAPPA) K[S][dy + 1][dx + 1] = v ? __ldg(kappa + (ro + dx)) : 0.f;
                 }
             }
         }
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         if (act) {
             const unsigned idx = (unsigned)k * nxy + col;
             float gs, cs;
-            const bool km = k > 0, kp = k + 1 < G.nz;
+            const bool km = k > 0 || A.halo_lo, kp = k + 1 < G.nz || A.halo_hi;
             if (inxy && km && kp)
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
             else
@@ -415,6 +417,24 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
     A.pfx = nopfx ? nullptr : pfx;
     A.box_lo = box_lo;
     A.box_hi = box_hi;
+    upd_select<UPD_FULL>(G, rp, ctl, A, s);
+    launches_add(1);
+}
+
+void launch_update_halo(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
+                        float* g, float* ht, float box_lo, float box_hi, float* pfx, bool halo_lo, bool halo_hi,
+                        cudaStream_t s) {
+    UpdArgs A = {};
+    A.xa = xa;
+    A.xb = xb;
+    A.dl = dl;
+    A.g = g;
+    A.ht = ht;
+    A.pfx = pfx;
+    A.box_lo = box_lo;
+    A.box_hi = box_hi;
+    A.halo_lo = halo_lo;
+    A.halo_hi = halo_hi;
     upd_select<UPD_FULL>(G, rp, ctl, A, s);
     launches_add(1);
 }

@@ -69,7 +69,8 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "ct_reg_grad",
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
-           "oslalm_profile", "ct_count_nnz"]
+           "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
+           "oslalm_zslab_solve"]
 
 _lib = None
 
@@ -92,6 +93,11 @@ def load():
     L.ct_reg_grad.argtypes = [vp, P(ct_reg_desc), vp, vp, vp, vp, vp]
     L.ct_kappa_weights.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.ct_fbp.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.ct_zslab_range.argtypes = [vp, ctypes.c_int, ctypes.c_int, P(ctypes.c_int), P(ctypes.c_int)]
+    L.oslalm_zslab_workspace_size.argtypes = [vp, P(oslalm_params), ctypes.c_int, ctypes.c_int, P(ctypes.c_size_t)]
+    L.ct_sqs_diag_zslab.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, vp, P(vp), P(vp), ctypes.c_size_t, vp]
+    L.oslalm_zslab_solve.argtypes = [vp, vp, vp, P(ct_reg_desc), P(vp), P(oslalm_params), P(oslalm_state),
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, P(vp), ctypes.c_size_t, vp]
     L.oslalm_workspace_size.argtypes = [vp, P(oslalm_params), vp, P(ctypes.c_size_t)]
     L.oslalm_relaxed_solve.argtypes = [vp, vp, vp, P(ct_reg_desc), vp, vp, P(oslalm_params), P(oslalm_state),
                                        ctypes.c_int, vp, P(ctypes.c_double), vp, vp, ctypes.c_size_t, vp]
@@ -111,7 +117,8 @@ def load():
     for name in ("ct_geom_create", "ct_forward", "ct_back", "ct_sqs_diag", "ct_kappa_weights", "ct_fbp", "ct_reg_grad",
                  "oslalm_workspace_size",
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
-                 "oslalm_profile", "ct_count_nnz"):
+                 "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
+                 "ct_sqs_diag_zslab", "oslalm_zslab_solve"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -283,3 +290,37 @@ def ct_dist_destroy(h):
 
 def ct_launch_count():
     return load().ct_launch_count()
+
+
+# ----------------------------------------------------------------- z-slab decomposition
+def ct_zslab_range(geom, rank, world):
+    z0, nz = ctypes.c_int(), ctypes.c_int()
+    _check(load().ct_zslab_range(geom, int(rank), int(world), ctypes.byref(z0), ctypes.byref(nz)))
+    return z0.value, nz.value
+
+
+def oslalm_zslab_workspace_size(geom, p, rank, world):
+    n = ctypes.c_size_t()
+    _check(load().oslalm_zslab_workspace_size(geom, ctypes.byref(p), int(rank), int(world), ctypes.byref(n)))
+    return n.value
+
+
+def _ptr_array(ts):
+    return (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+def ct_sqs_diag_zslab(geom, w, d_outs, workspaces, world, dist=None, stream=None):
+    nbytes = min(t.numel() * t.element_size() for t in workspaces)
+    _check(load().ct_sqs_diag_zslab(geom, _ptr(w), len(d_outs), int(world), dist, _ptr_array(d_outs),
+                                    _ptr_array(workspaces), nbytes, _stream(stream)))
+
+
+def oslalm_zslab_solve(geom, y, w, reg, d_ls, p, states, n_subiters, workspaces, world, dist=None, stream=None):
+    """states: a list of oslalm_state (one per local slab); their k is advanced."""
+    arr = (oslalm_state * len(states))(*states)
+    nbytes = min(t.numel() * t.element_size() for t in workspaces)
+    _check(load().oslalm_zslab_solve(geom, _ptr(y), _ptr(w), ctypes.byref(reg), _ptr_array(d_ls), ctypes.byref(p),
+                                     arr, len(states), int(world), int(n_subiters), dist, _ptr_array(workspaces),
+                                     nbytes, _stream(stream)))
+    for i, s_ in enumerate(states):
+        s_.k = arr[i].k

@@ -450,3 +450,72 @@ def test_nccl_sharded_path_world1_matches_single_gpu(C, kind):
                 assert rel(b, a) <= 1e-5   # same arithmetic, different FMA contraction / order
     finally:
         C.ct_dist_destroy(d)
+
+
+@pytest.mark.parametrize("kind,world", [("helical_arc", 2), ("helical_arc", 3), ("axial_flat", 2),
+                                        ("helical_fine", 3), ("fan2d_arc", 1)])
+def test_zslab_decomposition_matches_single_gpu(C, kind, world):
+    """the z-slab decomposition with `world` slabs driven by one
+    process (partial projections summed on the device, halos copied) equals the
+    fused single-GPU solve: D_L, and x, g, htilde after 7 sub-iterations split
+    over two calls."""
+    from paper_1512_04564_b200.recon import Recon
+    pb = synthetic_problem(tiny(kind), M=3)
+    ref = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
+    ref.compute_DL()
+    ref.run(7)
+    want = [host(ref.x), host(ref.g), host(ref.htilde), host(ref.dl)]
+    ref.close()
+    g = pb["geom"]
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        p = C.params(3, 1.999)
+        reg = C.reg_desc(pb["reg"]["potential"], pb["reg"]["delta"], pb["reg"]["betas"], pb["reg"]["n_dirs"])
+        y, w = dev(pb["y"]), dev(pb["w"])
+        xs, gs, hs, dls, wss, sts = [], [], [], [], [], []
+        nb = max(C.oslalm_zslab_workspace_size(h, p, r, world) for r in range(world))
+        for r in range(world):
+            z0, nz = C.ct_zslab_range(h, r, world)
+            xs.append(dev(pb["x0"][z0:z0 + nz]))
+            gs.append(torch.zeros_like(xs[-1]))
+            hs.append(torch.zeros_like(xs[-1]))
+            dls.append(torch.empty_like(xs[-1]))
+            wss.append(torch.empty(nb, dtype=torch.uint8, device="cuda"))
+            sts.append(C.make_state(xs[-1], gs[-1], hs[-1], 0))
+        C.ct_sqs_diag_zslab(h, w, dls, wss, world)
+        assert rel(host(torch.cat(dls)), want[3]) <= 1e-5
+        C.oslalm_zslab_solve(h, y, w, reg, dls, p, sts, 3, wss, world)
+        C.oslalm_zslab_solve(h, y, w, reg, dls, p, sts, 4, wss, world)
+        assert all(s_.k == 7 for s_ in sts)
+        for got, exp in zip((torch.cat(xs), torch.cat(gs), torch.cat(hs)), want):
+            assert rel(host(got), exp) <= 1e-5, rel(host(got), exp)
+    finally:
+        C.ct_geom_destroy(h)
+
+
+def test_zslab_nccl_world1(C):
+    """The z-slab driver's NCCL path (one slab per process, ncclAllReduce of the
+    partial projections, halo send/recv) on a world-1 communicator."""
+    pb = synthetic_problem(tiny("helical_arc"), M=3)
+    from paper_1512_04564_b200.recon import Recon
+    ref = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
+    ref.compute_DL()
+    ref.run(5)
+    want = host(ref.x)
+    ref.close()
+    g = pb["geom"]
+    h = C.ct_geom_create(C.geom_desc(g))
+    d = C.ct_dist_create(0, 1, C.ct_nccl_unique_id(), 0)
+    try:
+        p = C.params(3, 1.999)
+        reg = C.reg_desc(pb["reg"]["potential"], pb["reg"]["delta"], pb["reg"]["betas"], pb["reg"]["n_dirs"])
+        x = dev(pb["x0"])
+        gg, hh, dl = torch.zeros_like(x), torch.zeros_like(x), torch.empty_like(x)
+        ws = torch.empty(C.oslalm_zslab_workspace_size(h, p, 0, 1), dtype=torch.uint8, device="cuda")
+        C.ct_sqs_diag_zslab(h, dev(pb["w"]), [dl], [ws], 1, dist=d)
+        st = C.make_state(x, gg, hh, 0)
+        C.oslalm_zslab_solve(h, dev(pb["y"]), dev(pb["w"]), reg, [dl], p, [st], 5, [ws], 1, dist=d)
+        assert rel(host(x), want) <= 1e-5
+    finally:
+        C.ct_dist_destroy(d)
+        C.ct_geom_destroy(h)
