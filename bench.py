@@ -252,8 +252,14 @@ def run_cuda(args):
         cdist = C.ct_dist_create(0, 1, C.ct_nccl_unique_id(), local)
 
     stream = torch.cuda.current_stream(dev)
-    rec = Recon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], device=local,
-                dist=cdist)
+    if args.decomp == "zslab":
+        # z-slab volume decomposition: this rank's planes, partial-projection all-reduce
+        from paper_1512_04564_b200.recon import ZslabRecon
+        rec = ZslabRecon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], rank=rank,
+                         world=world, device=local, dist=cdist)
+    else:
+        rec = Recon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], device=local,
+                    dist=cdist)
     rec.compute_DL()
     torch.cuda.synchronize()
 
@@ -291,15 +297,21 @@ def run_cuda(args):
     clocks = sampler.stop() if sampler else None
     value = M * args.steps / (ms / 1000.0)
 
-    # ---- per-kernel device times (eager launches with CUDA events, same stream)
-    kms = C.oslalm_profile(rec.h, rec.y, rec.w, rec.reg, rec.kappa, rec.dl, rec.params, rec.state, M, rec.ws,
-                           dist=cdist, stream=stream)
+    # ---- per-kernel device times (eager launches with CUDA events, same stream); the z-slab
+    # path reports them from a full-volume view-path profile of the same configuration
+    prec = rec
+    if args.decomp == "zslab":
+        prec = Recon(g, inputs["reg"], cfg["solver"], inputs["y"], inputs["w"], inputs["x0"], device=local)
+        prec.compute_DL()
+        prec.run(M)
+    kms = C.oslalm_profile(prec.h, prec.y, prec.w, prec.reg, prec.kappa, prec.dl, prec.params, prec.state, M,
+                           prec.ws, dist=cdist if prec is rec else None, stream=stream)
     kms = [max_over_ranks(v) for v in kms]
     # nonzeros of A per subset (2 FLOP each: DESIGN.md §8)
     nnz = 0
     for m in range(M):
         st_, sd_, ct_ = subset_views(g["na"], M, m)
-        nnz += C.ct_count_nnz(rec.h, C.views(st_, sd_, ct_))
+        nnz += C.ct_count_nnz(prec.h, C.views(st_, sd_, ct_))
     nnz_sub = nnz / M
 
     # ---- e2e: through the public API with host buffers (pinned), every step: step i's y, w
@@ -343,7 +355,7 @@ def run_cuda(args):
     names = ["update (stencil + x-update)", "forward + weighted residual", "back-projection + g/htilde",
              "other (all-reduce, k advance)"]
     dom = max(range(3), key=lambda q: kms[q])
-    nvox = rec.x.numel()
+    nvox = prec.x.numel()
     vm = (g["na"] + M - 1) // M
     nt = g["nt"] if g["dim"] == 3 else 1
     rm = vm * nt * g["ns"]
@@ -396,10 +408,12 @@ def run_cuda(args):
         "data": "synthetic (seeded random-ellipsoid phantom, analytic line integrals, Poisson%s noise)" %
                 (" + electronic" if cfg["noise"]["sigma"] > 0 else ""),
         "config": {"workload": WORKLOADS[args.config], "config": args.config, "subsets": M,
-                   "sub_iters_per_step": M, "volume": list(rec.x.shape), "views": g["na"],
-                   "parallelism": "views of each subset sharded over %d GPU(s), NCCL all-reduce of zeta" % world
-                   if world > 1 else ("1 GPU, multi-GPU code path on a world-1 NCCL communicator"
-                                      if cdist is not None else "1 GPU"),
+                   "sub_iters_per_step": M, "volume": list(prec.x.shape), "views": g["na"],
+                   "parallelism": ("z-slabs of the volume over %d GPU(s), NCCL all-reduce of the partial "
+                                   "projections" % world) if args.decomp == "zslab" else
+                                  ("views of each subset sharded over %d GPU(s), NCCL all-reduce of zeta" % world
+                                   if world > 1 else ("1 GPU, multi-GPU code path on a world-1 NCCL communicator"
+                                                      if cdist is not None else "1 GPU")),
                    "l2": "no flush: per-sub-iteration working set %.0f MB > 126 MB L2" % work_mb},
         "roofline": roof, "kernels": kernels, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clocks,
@@ -418,6 +432,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--decomp", default="views", choices=["views", "zslab"],
+                    help="multi-GPU decomposition: views of each subset (default) or z-slabs of the volume")
     ap.add_argument("--dist-path", action="store_true",
                     help="N=1 only: run the multi-GPU code path on a world-1 NCCL communicator")
     ap.add_argument("--no-cpu-baseline", action="store_true")

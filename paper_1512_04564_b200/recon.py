@@ -153,3 +153,57 @@ class HostPipeline:
     def finish(self):
         """Make the compute stream wait for every outstanding copy."""
         self.comp.wait_stream(self.copy)
+
+
+class ZslabRecon:
+    """Rank `rank` of a z-slab decomposition (oslalm_zslab_solve):
+    holds this rank's planes of x, g, htilde, D_L and the full y, w.  Same
+    run / compute_DL / x interface as Recon (allocation + C-ABI calls only).
+    dist: a ct_dist communicator for world > 1 (one process per GPU)."""
+
+    def __init__(self, geom, reg, solver, y, w, x0, rank=0, world=1, device=0, dist=None, stream=None):
+        self.dev = torch.device("cuda", device)
+        self.geom = geom
+        self.h = C.ct_geom_create(C.geom_desc(geom), device)
+        self.rank, self.world, self.dist, self.stream = rank, world, dist, stream
+        self.z0, self.nz = C.ct_zslab_range(self.h, rank, world)
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.y = torch.as_tensor(y).to(**f32).contiguous()
+        self.w = torch.as_tensor(w).to(**f32).contiguous()
+        self.x = torch.as_tensor(x0).to(**f32)[self.z0:self.z0 + self.nz].contiguous().clone()
+        self.g = torch.zeros_like(self.x)
+        self.htilde = torch.zeros_like(self.x)
+        self.dl = torch.empty_like(self.x)
+        self.reg = C.reg_desc(reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"],
+                              reg.get("curvature", "huber"), reg.get("q", 1.2))
+        self.params = C.params(solver["M"], solver["alpha"],
+                               C.RHO_FIXED if solver.get("rho_mode") == "fixed" else C.RHO_CONTINUATION,
+                               solver.get("rho_fixed", 0.0),
+                               C.INIT_FULL if solver.get("init_grad") == "full" else C.INIT_LAST_SUBSET,
+                               solver.get("box_lo", 0.0), solver.get("box_hi", math.inf),
+                               C.SIMPLE if solver.get("variant") == "simple" else C.PROPOSED)
+        self.ws = torch.empty(C.oslalm_zslab_workspace_size(self.h, self.params, rank, world), dtype=torch.uint8,
+                              device=self.dev)
+        self.state = C.make_state(self.x, self.g, self.htilde, 0)
+        self.have_dl = False
+
+    def compute_DL(self):
+        C.ct_sqs_diag_zslab(self.h, self.w, [self.dl], [self.ws], self.world, dist=self.dist, stream=self.stream)
+        self.have_dl = True
+        return self.dl
+
+    def run(self, n_subiters):
+        if not self.have_dl:
+            self.compute_DL()
+        C.oslalm_zslab_solve(self.h, self.y, self.w, self.reg, [self.dl], self.params, [self.state], n_subiters,
+                             [self.ws], self.world, dist=self.dist, stream=self.stream)
+        return self.x
+
+    @property
+    def k(self):
+        return self.state.k
+
+    def close(self):
+        if self.h is not None:
+            C.ct_geom_destroy(self.h)
+            self.h = None
