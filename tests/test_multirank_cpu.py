@@ -90,3 +90,86 @@ def test_two_rank_gloo_sum_of_partial_backprojections_equals_full_subset():
         full = M * P.back(g, r, (st, sd, cnt))
         assert np.allclose(out[m], full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
     assert uid == bytes(range(128)) and tmax == 2.0
+
+
+def _slab(g, nz, rank, world):
+    """Planes [z0, z0 + n) of rank `rank` (the partition of ct_zslab_range) and their geometry."""
+    z0 = rank * nz // world
+    n = (rank + 1) * nz // world - z0
+    gs = dict(g, nz=n, offset_z=g["offset_z"] + (z0 + (n - 1) / 2.0 - (nz - 1) / 2.0) * g["dz"])
+    return z0, n, gs
+
+
+def _zslab_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import projector as P
+        from tests.geoms import tiny
+        from tests.problems import synthetic_problem
+        pb = synthetic_problem(tiny("helical_arc"), M=4)
+        g = pb["geom"]
+        nz = g["nz"]
+        z0, n, gs = _slab(g, nz, rank, world)
+        x = pb["x0"][z0:z0 + n]
+        # partial projection of the slab, summed over the ranks (the NCCL all-reduce's job)
+        part = torch.from_numpy(P.forward(gs, x, (0, 1, g["na"])))
+        dist.all_reduce(part)
+        # halo planes from the neighbours (ncclSend/Recv on the GPU path), then the stencil
+        lo = torch.zeros(x.shape[1:], dtype=torch.float64)
+        hi = torch.zeros(x.shape[1:], dtype=torch.float64)
+        reqs = []
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(x[0])), rank - 1))
+            reqs.append(dist.irecv(lo, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(x[-1])), rank + 1))
+            reqs.append(dist.irecv(hi, rank + 1))
+        for r_ in reqs:
+            r_.wait()
+        planes = ([lo.numpy()] if rank > 0 else []) + list(x) + ([hi.numpy()] if rank + 1 < world else [])
+        ext = np.stack(planes)
+        a = 1 if rank > 0 else 0
+        ge = dict(gs, nz=ext.shape[0], offset_z=gs["offset_z"] + ((1 if rank + 1 < world else 0) - a) * g["dz"] / 2.0)
+        _, gr, cv = P.reg(ge, "hyperbola", 0.01, pb["reg"]["betas"], 13, ext)
+        gr, cv = gr[a:a + n], cv[a:a + n]
+        got = [None] * world
+        dist.all_gather_object(got, (z0, gr, cv))
+        if rank == 0:
+            q.put((part.numpy(), got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_zslab_gloo_partial_projections_and_halo_stencil(world):
+    """z-slab decomposition host logic with gloo ranks: the slabs'
+    partial projections sum to the full projection, and the stencil of a slab
+    extended by the neighbours' halo planes equals the full volume's stencil."""
+    from oracle import projector as P
+    from tests.geoms import tiny
+    from tests.problems import synthetic_problem
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zslab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    proj, parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pb = synthetic_problem(tiny("helical_arc"), M=4)
+    g = pb["geom"]
+    full = P.forward(g, pb["x0"], (0, 1, g["na"]))
+    assert np.allclose(proj, full, rtol=1e-12, atol=1e-12 * np.abs(full).max())
+    _, gr, cv = P.reg(g, "hyperbola", 0.01, pb["reg"]["betas"], 13, pb["x0"])
+    covered = 0
+    for z0, gsl, csl in parts:
+        n = gsl.shape[0]
+        assert np.allclose(gsl, gr[z0:z0 + n], rtol=1e-12, atol=1e-15)
+        assert np.allclose(csl, cv[z0:z0 + n], rtol=1e-12, atol=1e-15)
+        covered += n
+    assert covered == g["nz"]
