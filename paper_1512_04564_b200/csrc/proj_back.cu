@@ -28,19 +28,23 @@ constexpr int BK_BS = 32 * BK_Y;
 constexpr int BK_KZ_DEFAULT = 24;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24 | 32)
 constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 at KZ = 16 (more rows => several passes)
 
-// 2-D back-projection: thread = one pixel; per view one footprint and the
-// F1-weighted sum over the <= kMaxCells cells it covers.
-template <bool ARC, int EPI>
-__global__ void __launch_bounds__(BK_BS)
+// 2-D back-projection: thread = one pixel and every VS-th view of the subset
+// (VS > 1 for small images, so that a 128 x 128 image still fills the GPU);
+// per view one footprint and the F1-weighted sum over the <= kMaxCells cells it
+// covers; the VS partial sums are added in a fixed order (deterministic).
+template <bool ARC, int EPI, int VS>
+__global__ void __launch_bounds__(BK_BS * VS)
 k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
+    __shared__ float red[VS][BK_Y][32];
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
-    if (i >= G.nx || j >= G.ny) return;
+    const int part = threadIdx.z;
+    const bool act = i < G.nx && j < G.ny;
     const Views V = select_views(ctl, vsel);
     float acc = 0.f;
-    for (int vi = 0; vi < V.count; vi++) {
+    for (int vi = part; act && vi < V.count; vi += VS) {
         const int v = V.start + vi * V.stride;
         const float4 vw = __ldg(&vtab[v]);
         Footprint f;
@@ -57,6 +61,15 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         }
         acc = fmaf(f.lxy, rs, acc);
     }
+    if (VS > 1) {
+        red[part][threadIdx.y][threadIdx.x] = acc;
+        __syncthreads();
+        if (part != 0) return;
+        acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < VS; q++) acc += red[q][threadIdx.y][threadIdx.x];
+    }
+    if (!act) return;
     const size_t idx = (size_t)j * G.nx + i;
     const float z = scale * acc;
     if (EPI == BK_WRITE) {
@@ -310,13 +323,24 @@ static void back3_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl
 template <bool ARC>
 static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
                            float scale, int epi, float* out, float* g, float* ht, cudaStream_t s) {
-    dim3 block(32, BK_Y);
     dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, 1);
+    // split the views over 4 threads per pixel when the image has fewer blocks than ~4 per SM
+    if ((long long)grid.x * grid.y < 148LL * 4) {
+        dim3 block(32, BK_Y, 4);
+        switch (epi) {
+            case BK_WRITE: k_back2<ARC, BK_WRITE, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_ACCUM: k_back2<ARC, BK_ACCUM, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_INIT: k_back2<ARC, BK_INIT, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            default: k_back2<ARC, BK_UPDATE, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        }
+        return;
+    }
+    dim3 block(32, BK_Y, 1);
     switch (epi) {
-        case BK_WRITE: k_back2<ARC, BK_WRITE><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        case BK_ACCUM: k_back2<ARC, BK_ACCUM><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        case BK_INIT: k_back2<ARC, BK_INIT><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        default: k_back2<ARC, BK_UPDATE><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_WRITE: k_back2<ARC, BK_WRITE, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_ACCUM: k_back2<ARC, BK_ACCUM, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_INIT: k_back2<ARC, BK_INIT, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        default: k_back2<ARC, BK_UPDATE, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
     }
 }
 
