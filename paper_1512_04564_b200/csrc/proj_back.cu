@@ -92,8 +92,11 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
 // rs(t) = sum_q F[q] r[t][sw + q] (L_z(s, t) folded in when LZ), stored with
 // the running sum as cs[o] = (sum_{t' < t} rs, rs(t)).  The next row's W
 // gathers are issued before the current row's FMAs (software pipelining).
+#ifndef BK_WMAX
+#define BK_WMAX 6      // widest register window of detector columns (wider footprints: general loop)
+#endif
 template <bool ARC, bool LZ, int W>
-__device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[8], const float* __restrict__ pr,
+__device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WMAX], const float* __restrict__ pr,
                                           int sw, int tw, int n, float2* __restrict__ cs, float& run) {
     float a[W], b[W];
 #pragma unroll
@@ -197,16 +200,16 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         const int nc = shi - slo + 1;
         if (nc <= 0) continue;
         const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
-        // warp-uniform window of W = 4, 6 or 8 detector columns [sw, sw + W - 1] inside the
+        // warp-uniform window of W = 4 or BK_WMAX detector columns [sw, sw + W - 1] inside the
         // detector (F1 is exactly 0 outside [u0, u3]); wider footprints take a general loop
         const int ncmax = __reduce_max_sync(__activemask(), nc);
-        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= 6 && G.ns >= 6) ? 6 : (ncmax <= 8 && G.ns >= 8) ? 8 : 0;
+        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= BK_WMAX && G.ns >= BK_WMAX) ? BK_WMAX : 0;
         const int sw = W ? max(min(slo, G.ns - W), 0) : slo;
-        float F[8];
+        float F[BK_WMAX];
         {
             float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
+            for (int q = 0; q < BK_WMAX; q++) {
                 if (q < 4 || q < W) {
                     const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
                     F[q] = (Tn - Tprev) * f.lxy;
@@ -224,10 +227,8 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
             const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns + (unsigned)sw);
             if (W == 4) {
                 back_rows<ARC, LZ, 4>(G, F, pr, sw, tw, n, cs, run);
-            } else if (W == 6) {
-                back_rows<ARC, LZ, 6>(G, F, pr, sw, tw, n, cs, run);
-            } else if (W == 8) {
-                back_rows<ARC, LZ, 8>(G, F, pr, sw, tw, n, cs, run);
+            } else if (W == BK_WMAX) {
+                back_rows<ARC, LZ, BK_WMAX>(G, F, pr, sw, tw, n, cs, run);
             } else {
                 // wide footprint (near the source in steep geometries): F1 on the fly
                 for (int o = 0; o < n; o++) {
