@@ -249,20 +249,22 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
             cs[n * BK_BS] = make_float2(run, 0.f);
             // R(u) at voxel boundary u = B0 + k H: v = u - (tw + 1/2) in [-1/2, n - 1/2],
             // o = round(v) (magic number), frac = v + 1/2 - o in [0, 1]
-            const float sh = Bs - (float)tw;
+            // boundary q of the chunk sits at row unit B0 + (k0 + q) H; q is a compile-time
+            // constant after unrolling, so the position is one FFMA with an immediate
+            const float base = fmaf((float)k0, H, Bs - (float)tw);
             const float vmax = (float)n - 0.5f;
-            auto R = [&](int k) {
-                const float vv = fminf(fmaxf(fmaf((float)k, H, sh), -0.5f), vmax);
+            auto R = [&](int q) {
+                const float vv = fminf(fmaxf(fmaf((float)q, H, base), -0.5f), vmax);
                 const float rm = __fadd_rn(vv, 12582912.0f);
                 const int o = __float_as_int(rm) - 0x4B400000;
                 const float fr = (vv + 0.5f) - (rm - 12582912.0f);
                 const float2 c = cs[o * BK_BS];
                 return fmaf(fr, c.y, c.x);
             };
-            float Rlo = R(k0);
+            float Rlo = R(0);
 #pragma unroll
             for (int q = 0; q < BK_KZ; q++) {
-                const float Rhi = R(k0 + q + 1);
+                const float Rhi = R(q + 1);
                 acc[q] += Rhi - Rlo;
                 Rlo = Rhi;
             }
