@@ -13,6 +13,13 @@ import torch
 from . import ctrecon as C
 
 
+def _variant(solver):
+    v = solver.get("variant", "proposed")
+    if v not in ("proposed", "simple"):
+        raise ValueError("solver variant must be 'proposed' (Algorithm 1) or 'simple' (Algorithm 2), got %r" % (v,))
+    return C.SIMPLE if v == "simple" else C.PROPOSED
+
+
 class Recon:
     def __init__(self, geom, reg, solver, y, w, x0, kappa=None, device=0, dist=None, stream=None):
         """geom/reg/solver: dicts as in synth/configs.py; y, w: (na, nt, ns);
@@ -38,7 +45,7 @@ class Recon:
                                solver.get("rho_fixed", 0.0),
                                C.INIT_FULL if solver.get("init_grad") == "full" else C.INIT_LAST_SUBSET,
                                solver.get("box_lo", 0.0), solver.get("box_hi", math.inf),
-                               C.SIMPLE if solver.get("variant") == "simple" else C.PROPOSED)
+                               _variant(solver))
         nbytes = C.oslalm_workspace_size(self.h, self.params, dist)
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
         self.state = C.make_state(self.x, self.g, self.htilde, 0)
@@ -181,7 +188,7 @@ class ZslabRecon:
                                solver.get("rho_fixed", 0.0),
                                C.INIT_FULL if solver.get("init_grad") == "full" else C.INIT_LAST_SUBSET,
                                solver.get("box_lo", 0.0), solver.get("box_hi", math.inf),
-                               C.SIMPLE if solver.get("variant") == "simple" else C.PROPOSED)
+                               _variant(solver))
         self.ws = torch.empty(C.oslalm_zslab_workspace_size(self.h, self.params, rank, world), dtype=torch.uint8,
                               device=self.dev)
         self.state = C.make_state(self.x, self.g, self.htilde, 0)

@@ -349,6 +349,43 @@ def test_errors_have_no_side_effects(C):
         with pytest.raises(C.CtError) as e:
             C.ct_geom_create(C.geom_desc(bad_geom))
         assert e.value.status == C.CT_E_CONFIG
+        for bad_g in (tiny("helical_arc", nz=1537), tiny("helical_arc", nx=70000, ny=70000)):
+            with pytest.raises(C.CtError) as e:
+                C.ct_geom_create(C.geom_desc(bad_g))
+            assert e.value.status == C.CT_E_CONFIG
+        # variant / curvature / q-GGMRF exponent outside their ranges, before any launch
+        for bad in (dict(variant="bogus"),):
+            with pytest.raises(ValueError):
+                Recon(g, pb["reg"], dict(pb["solver"], **bad), pb["y"], pb["w"], pb["x0"]).run(1)
+        r = Recon(g, pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
+        r.compute_DL()
+        x_before = r.x.clone()
+        for reg in (C.reg_desc("qggmrf", 0.01, pb["reg"]["betas"], 4, "huber", 2.5),
+                    C.reg_desc("qggmrf", 0.01, pb["reg"]["betas"], 4, "huber", 0.5)):
+            r.reg = reg
+            with pytest.raises(C.CtError) as e:
+                r.run(2)
+            assert e.value.status == C.CT_E_CONFIG and r.k == 0 and torch.equal(r.x, x_before)
+        r.reg = C.reg_desc("hyperbola", 0.01, pb["reg"]["betas"], 4)
+        r.reg.curvature = 7
+        with pytest.raises(C.CtError) as e:
+            r.run(2)
+        assert e.value.status == C.CT_E_CONFIG and r.k == 0
+        r.params.variant = 5
+        r.reg = C.reg_desc("hyperbola", 0.01, pb["reg"]["betas"], 4)
+        with pytest.raises(C.CtError) as e:
+            r.run(2)
+        assert e.value.status == C.CT_E_CONFIG and r.k == 0
+        r.close()
+        # FBP needs a 360-degree orbit
+        hs = C.ct_geom_create(C.geom_desc(dict(g, orbit_deg=200.0)))
+        try:
+            ws = torch.empty(g["na"] * g["ns"] * 4, dtype=torch.uint8, device="cuda")
+            with pytest.raises(C.CtError) as e:
+                C.ct_fbp(hs, torch.zeros(P.proj_shape(g, g["na"]), device="cuda"), x, ws)
+            assert e.value.status == C.CT_E_CONFIG
+        finally:
+            C.ct_geom_destroy(hs)
         # empty view descriptor is a no-op
         C.ct_forward(h, x, C.views(0, 1, 0), p)
         assert float(p.min()) == 7.0
