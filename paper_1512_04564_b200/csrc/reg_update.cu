@@ -406,7 +406,6 @@ void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                    const float* g, float* ht, const float* kappa, float box_lo, float box_hi, float* pfx,
                    cudaStream_t s) {
-    static const int nopfx = env_int("CTR_UPD_NOPFX", 0);  // timing experiment only: skips the prefix
     UpdArgs A = {};
     A.xa = xa;
     A.xb = xb;
@@ -414,7 +413,7 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
     A.g = const_cast<float*>(g);
     A.ht = ht;
     A.kappa = kappa;
-    A.pfx = nopfx ? nullptr : pfx;
+    A.pfx = pfx;
     A.box_lo = box_lo;
     A.box_hi = box_hi;
     upd_select<UPD_FULL>(G, rp, ctl, A, s);
