@@ -374,6 +374,7 @@ def run_cuda(args):
                 "frac": achieved / pk["hbm_gbs"], "traffic": None, "kernel": names[dom],
                 "algorithmic": "24 B/voxel", "peak_source": pk["source"]}
     tfile = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
+    tr = {}
     if os.path.exists(tfile):
         try:
             with open(tfile) as f:
@@ -381,7 +382,7 @@ def run_cuda(args):
             key = {0: "update", 1: "forward", 2: "back"}[dom]
             roof["traffic"] = tr.get(key)
         except Exception:
-            pass
+            tr = {}
     # projector GB/s (algorithmic bytes: fwd reads x, y, w, writes r; back reads r, r/w g, htilde)
     fwd_bytes = 4.0 * nvox + 12.0 * rm / world
     back_bytes = 4.0 * rm / world + 16.0 * nvox
@@ -393,6 +394,12 @@ def run_cuda(args):
         "forward_fp32_frac": 2.0 * nnz_sub / world / (kms[1] / M / 1e3) / 1e12 / pk["fp32_tflops"],
         "back_fp32_frac": 2.0 * nnz_sub / world / (kms[2] / M / 1e3) / 1e12 / pk["fp32_tflops"],
     }
+    # projector HBM GB/s (the metric's second half): measured DRAM bytes per launch of the committed
+    # ncu capture (profiles/traffic_<config>.json, same kernels and config) over this run's kernel times
+    for key, q in (("forward", 1), ("back", 2), ("update", 0)):
+        if tr.get(key):
+            kernels[key + "_dram_gbs"] = tr[key] / (kms[q] / M / 1e3) / 1e9
+            kernels[key + "_dram_frac"] = kernels[key + "_dram_gbs"] / pk["hbm_gbs"]
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         from oracle import projector as P
