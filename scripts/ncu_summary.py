@@ -1,9 +1,9 @@
 """Summarise an ncu launch list + an ncu --set full capture into profiles/<tag>/.
 
-usage: python scripts/ncu_summary.py <tag> <launches.csv> <prof.ncu-rep> [bench.log]
+usage: python scripts/ncu_summary.py <tag> <launches.csv> <prof.ncu-rep> [bench.log] [config]
 Writes profiles/<tag>/summary.md, kernels.csv (per-kernel launch times) and
-profiles/traffic_c4.json (DRAM bytes per launch of the three hot kernels, read
-by bench.py's roofline.traffic).
+profiles/traffic_<config>.json (DRAM bytes per launch of the three hot kernels,
+read by bench.py's roofline.traffic; config defaults to c4).
 """
 import csv
 import io
@@ -53,7 +53,8 @@ def raw_metrics(rep):
 
 def main():
     tag, lpath, rep = sys.argv[1:4]
-    blog = sys.argv[4] if len(sys.argv) > 4 else None
+    blog = sys.argv[4] if len(sys.argv) > 4 and sys.argv[4] != "-" else None
+    cfg = sys.argv[5] if len(sys.argv) > 5 else "c4"
     od = os.path.join(ROOT, "profiles", tag)
     os.makedirs(od, exist_ok=True)
     lt = launch_table(lpath)
@@ -66,13 +67,15 @@ def main():
         for n, (c, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             f.write("%s,%d,%.1f,%.2f\n" % (n, c, t / 1e3, t / 1e3 / c))
     # the sub-iteration kernels of the solve (graph replays + profiled eager run)
-    sub = {k: v for k, v in agg.items() if k.startswith(("k_update", "k_advance")) or
-           (k.startswith("k_fwd3") and ",1,2,1>" in k) or (k.startswith("k_back3") and ",3,0," in k)}
+    # the solve's sub-iteration kernels: update, forward with the residual epilogue (MODE 1), back with
+    # the g/htilde epilogue (EPI 3), advance
+    sub = {k: v for k, v in agg.items() if k.startswith(("k_update<", "k_advance")) or
+           re.fullmatch(r"k_fwd3<\d,1,\d,1>|k_fwd2<\d,1>|k_back3<\d,3,0,\d+>|k_back2<\d,3,\d>", k)}
     tot = sum(v[1] for v in sub.values())
     lines = ["# ncu summary %s" % tag, "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
-             "`python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline` (c4).  Times are "
-             "cold-cache and serialised: compare shares, not absolutes.", "",
+             "`python bench.py --config %s --steps 1 --warmup 1 --no-e2e --no-cpu-baseline`.  Times are "
+             "cold-cache and serialised: compare shares, not absolutes." % cfg, "",
              "| sub-iteration kernel | launches | avg us | share of sub-iteration |", "|---|---|---|---|"]
     for n, (c, t) in sorted(sub.items(), key=lambda kv: -kv[1][1]):
         lines.append("| `%s` | %d | %.1f | %.1f%% |" % (n, c, t / 1e3 / c, 100 * t / tot))
@@ -111,7 +114,7 @@ def main():
             unit = metrics[0].get("dram__bytes_read.sum", "")
         except Exception:
             continue
-        key = "forward" if n.startswith("k_fwd3") else "back" if n.startswith("k_back") else \
+        key = "forward" if n.startswith(("k_fwd3", "k_fwd2")) else "back" if n.startswith("k_back") else \
             "update" if n.startswith("k_update") else None
         if key:
             traffic[key] = (rd, wr)
@@ -125,7 +128,7 @@ def main():
         tj[k] = rd * scale.get(units.get("dram__bytes_read.sum", "byte"), 1) + \
             wr * scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
     tj["units"] = "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum), capture %s" % tag
-    with open(os.path.join(ROOT, "profiles", "traffic_c4.json"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", "traffic_%s.json" % cfg), "w") as f:
         json.dump(tj, f, indent=1)
     lines += ["", "DRAM traffic per launch (bytes): " + json.dumps({k: v for k, v in tj.items() if k != "units"})]
     if blog and os.path.exists(blog):
