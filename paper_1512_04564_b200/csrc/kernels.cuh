@@ -23,8 +23,9 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
                 int pfx_stride = 0);  // > 0: xa is the float2 z-prefix array (3-D solve path)
 
 // z-prefix array of x+ for the 3-D forward (written by the update kernel):
-// per voxel column, float2 Q_k = (M_k, x_k) for k = 0..nz-1 and Q_nz = (P_nz, 0),
-// P_k = sum_{k'<k} x_k', M_k = P_k + x_k / 2 (the cumulative at the middle of voxel k).  Column stride in float2 units: nz + 1 rounded up to even.
+// per voxel column, float2 Q_k = (A_k, x_k) for k = 0..nz-1 and Q_nz = (P_nz, 0),
+// P_k = sum_{k'<k} x_k', A_k = P_k - (k - 1/2) x_k (the cumulative at voxel coordinate
+// f in [k - 1/2, k + 1/2] is A_k + f x_k).  Column stride in float2 units: nz + 1 rounded up to even.
 __host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 1) + 1) & ~1; }
 
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,

@@ -171,10 +171,11 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 // credited to the four detector columns with their own L = L_xy F1 (a voxel
 // column's footprint covers ~2.4 detector columns, so this removes most of the
 // redundant resampling of a one-column-per-warp walk).
-//   PFX (solve path): the x-update writes (M_k, x_k), M_k = P_k + x_k / 2 with
-//     P_k = sum_{k'<k} x_k', of every voxel column (float2, z-fastest, stride
-//     pfx_stride).  The magnified column is a piecewise-linear cumulative
-//     X(u) = H (P_k + frac x_k) = H (M_k + (f' - k) x_k) over row units u, and
+//   PFX (solve path): the x-update writes (A_k, x_k), A_k = P_k - (k - 1/2) x_k
+//     with P_k = sum_{k'<k} x_k', of every voxel column (float2, z-fastest,
+//     stride pfx_stride).  The magnified column is a piecewise-linear cumulative
+//     X(u) = H (P_k + (f' - k + 1/2) x_k) = H (A_k + f' x_k) over row units u
+//     (f' the voxel coordinate, k = round(f')), and
 //     the exact F2-weighted row sum is X(t+1) - X(t): RPL interpolations (one
 //     8-byte gather each) per lane plus one shuffle, no per-voxel loop, no
 //     divergence.
@@ -324,7 +325,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                                 const float ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), -0.5f), fnz - 0.5f);
                                 const float rt = __fadd_rn(ft, 12582912.0f);
                                 const float2 qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
-                                const float xtop = fmaf(ft - (rt - 12582912.0f), qt.y, qt.x);
+                                const float xtop = fmaf(ft, qt.y, qt.x);
                                 eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), xtop);
                             } else {
                                 eG = make_float4(f.B0, f.H, __int_as_float(j * G.nx + i), 0.f);
@@ -346,7 +347,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const int col = __float_as_int(q.z);
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
-                        // X(u) = H (M_k + (f' - k) x_k), M_k = P_k + x_k / 2, f' = (u - B0)/H - 1/2,
+                        // X(u) = H (A_k + f' x_k), A_k = P_k - (k - 1/2) x_k, f' = (u - B0)/H - 1/2,
                         // k = round(f') (1.5*2^23 magic number; f' clamped to [-1/2, nz - 1/2],
                         // where either rounding of a tie gives the same X: X is continuous and
                         // Q_nz = (P_nz, 0)), at the lane's RPL lower row boundaries; the upper
@@ -360,7 +361,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             f = fminf(fmaxf(f, -0.5f), fnz - 0.5f);
                             const float rm = __fadd_rn(f, 12582912.0f);
                             const float2 qk = __ldg(Q + (cb2 + (unsigned)__float_as_int(rm)));
-                            Xp[r] = fmaf(f - (rm - 12582912.0f), qk.y, qk.x);
+                            Xp[r] = fmaf(f, qk.y, qk.x);
                         }
                         const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);
                         Xp[RPL] = lane == 31 ? q.w : xn;

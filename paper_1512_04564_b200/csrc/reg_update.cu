@@ -119,9 +119,10 @@ enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
 
 // z-prefix of the block's x+ columns (x+ staged in shared memory xs[k][lane]):
 // chunk totals are scanned across the NZC chunks and each thread writes the
-// entries of its chunk, (M_k, x_k) as float2 with M_k = P_k + x_k / 2 and
+// entries of its chunk, (A_k, x_k) as float2 with A_k = P_k - (k - 1/2) x_k and
 // P_k = sum_{k'<k} x_k' (z-fastest, column stride pfx_stride_of(G)), plus
-// (P_nz, 0) from the last chunk.
+// (P_nz, 0) from the last chunk: the cumulative at voxel coordinate f in
+// [k - 1/2, k + 1/2] is then one FFMA, A_k + f x_k.
 __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__ pfx, const float* xs, float* tot,
                                              float run, int c, int lane, bool act, unsigned col, int k0, int k1) {
     tot[c * 32 + lane] = run;
@@ -132,7 +133,7 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
     float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + (size_t)col * (size_t)pfx_stride_of(G);
     for (int k = k0; k < k1; k++) {
         const float xk = xs[k * 33 + lane];
-        pc[k] = make_float2(fmaf(0.5f, xk, P), xk);  // (M_k, x_k): prefix to the middle of voxel k
+        pc[k] = make_float2(fmaf(0.5f - (float)k, xk, P), xk);  // (A_k, x_k), one rounding
         P += xk;
     }
     if (k1 == G.nz) pc[G.nz] = make_float2(P, 0.f);  // (P_nz, 0)
