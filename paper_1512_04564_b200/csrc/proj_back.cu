@@ -90,7 +90,9 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
 
 // Row sums of one (voxel column, view) over a window of W detector columns:
 // rs(t) = sum_q F[q] r[t][sw + q] (L_z(s, t) folded in when LZ), stored with
-// the running sum as cs[o] = (sum_{t' < t} rs, rs(t)).  The next row's W
+// the running sum in affine form, cs[o] = (C_o - (o - 1/2) rs(t), rs(t)) with
+// C_o = sum_{t' < t} rs and o = t - tw, so that the cumulative at row
+// coordinate v in [o - 1/2, o + 1/2] is one FFMA, cs[o].x + v cs[o].y.  The next row's W
 // gathers are issued before the current row's FMAs (software pipelining).
 #ifndef BK_WMAX
 #define BK_WMAX 6      // widest register window of detector columns (wider footprints: general loop)
@@ -99,6 +101,7 @@ template <bool ARC, bool LZ, int W>
 __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WMAX], const float* __restrict__ pr,
                                           int sw, int tw, int n, float2* __restrict__ cs, float& run) {
     float a[W], b[W];
+    float ofs = 0.5f;   // 1/2 - o
 #pragma unroll
     for (int q = 0; q < W; q++) a[q] = __ldg(pr + q);
     for (int o = 0; o < n; o++) {
@@ -111,8 +114,9 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
             const float wq = LZ ? F[q] * ray_Lz<ARC>(G, sw + q, tw + o) : F[q];
             rs = fmaf(wq, a[q], rs);
         }
-        cs[o * BK_BS] = make_float2(run, rs);
+        cs[o * BK_BS] = make_float2(fmaf(ofs, rs, run), rs);
         run += rs;
+        ofs -= 1.f;
         pr = pn;
 #pragma unroll
         for (int q = 0; q < W; q++) a[q] = b[q];
@@ -131,8 +135,9 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
 //      with its running sum as float2 (cs_t, rs_t) in a per-thread
 //      shared-memory column;
 //   4. per voxel: the F2-weighted row sum is R(b_k+1) - R(b_k) with the
-//      piecewise-linear cumulative R(u) = cs_o + frac rs_o (one 8-byte shared
-//      load per voxel boundary, magic-number floor).
+//      piecewise-linear cumulative R(u) = A_o + v rs_o, A_o = cs_o - (o - 1/2) rs_o
+//      (one 8-byte shared load and one FFMA per voxel boundary, magic-number
+//      rounding).
 template <bool ARC, int EPI, bool LZ, int BK_KZ>
 #ifndef BK_RM24
 #define BK_RM24 40     // rows buffered per pass at KZ = 24 (41 x 128 float2 = 42 KB)
@@ -241,14 +246,15 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                         rs = fmaf(wq, __ldg(pr + q), rs);
                         Tprev = Tn;
                     }
-                    cs[o * BK_BS] = make_float2(run, rs);
+                    cs[o * BK_BS] = make_float2(fmaf(0.5f - (float)o, rs, run), rs);
                     run += rs;
                     pr += G.ns;
                 }
             }
             cs[n * BK_BS] = make_float2(run, 0.f);
             // R(u) at voxel boundary u = B0 + k H: v = u - (tw + 1/2) in [-1/2, n - 1/2],
-            // o = round(v) (magic number), frac = v + 1/2 - o in [0, 1]
+            // o = round(v) (magic number), R = cs[o].x + v cs[o].y (affine form above;
+            // cs[n] = (C_n, 0))
             // boundary q of the chunk sits at row unit B0 + (k0 + q) H; q is a compile-time
             // constant after unrolling, so the position is one FFMA with an immediate
             const float base = fmaf((float)k0, H, Bs - (float)tw);
@@ -257,9 +263,8 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 const float vv = fminf(fmaxf(fmaf((float)q, H, base), -0.5f), vmax);
                 const float rm = __fadd_rn(vv, 12582912.0f);
                 const int o = __float_as_int(rm) - 0x4B400000;
-                const float fr = (vv + 0.5f) - (rm - 12582912.0f);
                 const float2 c = cs[o * BK_BS];
-                return fmaf(fr, c.y, c.x);
+                return fmaf(vv, c.y, c.x);
             };
             float Rlo = R(0);
 #pragma unroll
