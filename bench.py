@@ -396,10 +396,15 @@ def run_cuda(args):
     }
     # projector HBM GB/s (the metric's second half): measured DRAM bytes per launch of the committed
     # ncu capture (profiles/traffic_<config>.json, same kernels and config) over this run's kernel times
+    # and the instruction-issue fraction: the capture's warp instructions per launch over this run's
+    # kernel time at one issue per cycle per SM sub-partition (148 SMs x 4 x max SM clock)
     for key, q in (("forward", 1), ("back", 2), ("update", 0)):
         if tr.get(key):
             kernels[key + "_dram_gbs"] = tr[key] / (kms[q] / M / 1e3) / 1e9
             kernels[key + "_dram_frac"] = kernels[key + "_dram_gbs"] / pk["hbm_gbs"]
+        wi = tr.get("warp_inst", {}).get(key)
+        if wi:
+            kernels[key + "_issue_frac"] = wi / (kms[q] / M / 1e3) / (N_SM * 4 * pk["sm_max_mhz"] * 1e6)
     cb = None
     if world == 1 and not args.no_cpu_baseline:
         from oracle import projector as P

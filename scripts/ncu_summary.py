@@ -100,7 +100,7 @@ def main():
               "| kernel | " + " | ".join(w.split(".")[0].replace("__", ".") + ("" if "pct" not in w else " %")
                                        for w in want) + " |",
               "|---" * (len(want) + 1) + "|"]
-    traffic = {}
+    traffic, inst = {}, {}
     for d in metrics:
         n = short(d.get("Kernel Name", ""))
         vals = []
@@ -118,6 +118,10 @@ def main():
             "update" if n.startswith("k_update") else None
         if key:
             traffic[key] = (rd, wr)
+            try:
+                inst[key] = float(d["smsp__inst_executed.sum"].replace(",", ""))
+            except Exception:
+                pass
     units = dict(zip(list(csv.reader(io.StringIO(subprocess.run(
         ["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)))[0],
         list(csv.reader(io.StringIO(subprocess.run(
@@ -128,9 +132,12 @@ def main():
         tj[k] = rd * scale.get(units.get("dram__bytes_read.sum", "byte"), 1) + \
             wr * scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
     tj["units"] = "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum), capture %s" % tag
+    if inst:
+        tj["warp_inst"] = inst   # smsp__inst_executed.sum per launch (bench.py: issue fraction)
     with open(os.path.join(ROOT, "profiles", "traffic_%s.json" % cfg), "w") as f:
         json.dump(tj, f, indent=1)
-    lines += ["", "DRAM traffic per launch (bytes): " + json.dumps({k: v for k, v in tj.items() if k != "units"})]
+    lines += ["", "DRAM traffic per launch (bytes): " + json.dumps({k: v for k, v in tj.items()
+                                                                 if k not in ("units", "warp_inst")})]
     if blog and os.path.exists(blog):
         for line in open(blog):
             if line.startswith("{"):
