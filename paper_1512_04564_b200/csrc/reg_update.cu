@@ -145,8 +145,9 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 // planes lives in a register ring: plane k+2 and D_L, g, htilde of voxel k+1
 // are fetched at the top of step k and first touched one step later (a full
 // stencil of latency hiding); the march is unrolled by 4 so the ring slots are
-// compile-time.  Interior columns and planes take the predicate-free stencil
-// (warp-uniform except in the edge warps); the JPB rows of a block share their
+// compile-time.  Interior planes of warps without an edge column take the
+// predicate-free stencil (a warp-uniform choice: an edge warp runs the checked
+// stencil on all its lanes instead of both paths); the JPB rows of a block share their
 // x rows in L1.  32-bit element offsets (nvox < 2^32, ct_geom_create).
 //   UPD_FULL (Algorithm 1 lines 4-5, the solve path): x+ and htilde_partial in
 //     the boundary layout (coalesced over i); with pfx the z-prefix of x+.
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     const float idel = rp.inv_delta, del = rp.delta;
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
     const bool inxy = act && im && ip && jm && jp;
+    const bool wfast = __all_sync(0xffffffffu, !act || inxy);   // warp-uniform stencil path (no divergence)
     const unsigned nx = (unsigned)G.nx, nxy = (unsigned)G.nxy;
     const unsigned col = act ? (unsigned)j * nx + (unsigned)i : 0u;
     const int k0 = c * A.CZ, k1 = min(G.nz, k0 + A.CZ);
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
             const unsigned idx = (unsigned)k * nxy + col;
             float gs, cs;
             const bool km = k > 0 || A.halo_lo, kp = k + 1 < G.nz || A.halo_hi;
-            if (inxy && km && kp)
+            if (wfast && km && kp)
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
             else
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
