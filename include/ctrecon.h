@@ -293,6 +293,15 @@ ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state*
  * pi/(alpha(k+1)) sqrt(1 - (pi/(2 alpha (k+1)))^2). */
 double oslalm_rho(int64_t k, double alpha);
 
+/* Host -> device copy of the views v of a sinogram-shaped array (y or w):
+ * host and dev are both (na, nt, ns) float32 (host: pinned memory for an
+ * asynchronous copy), and view rows start + i*stride, i < count, of host are
+ * copied to the same rows of dev on stream s (one strided 2-D copy; other
+ * rows untouched).  Lets a caller stream a subset's data ahead of the
+ * sub-iteration that reads it (Algorithm 1 line 6 touches views of subset m
+ * only).  Errors: CT_E_CONFIG (NULL), CT_E_SHAPE (views), CT_E_CUDA. */
+ct_status ct_sino_upload(const ct_geom* g, const float* host, ct_views v, float* dev, ct_stream s);
+
 /* Synchronise the stream and report deferred asynchronous errors. */
 ct_status ct_sync(ct_stream s);
 

@@ -685,6 +685,19 @@ extern "C" ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const os
     return check_async();
 }
 
+extern "C" ct_status ct_sino_upload(const ct_geom* g, const float* host, ct_views v, float* dev, ct_stream s) {
+    if (!g || !host || !dev) return fail(CT_E_CONFIG, "ct_sino_upload: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    if (v.count == 0) return CT_OK;
+    DeviceGuard guard(g->device);
+    const size_t row = (size_t)g->d.nt * (size_t)g->d.ns;   // floats per view
+    const size_t off = (size_t)v.start * row, pitch = (size_t)v.stride * row * sizeof(float);
+    CT_CUDA(cudaMemcpy2DAsync(dev + off, pitch, host + off, pitch, row * sizeof(float), (size_t)v.count,
+                              cudaMemcpyHostToDevice, (cudaStream_t)s));
+    return CT_OK;
+}
+
 extern "C" ct_status ct_sync(ct_stream s) {
     CT_CUDA(cudaStreamSynchronize((cudaStream_t)s));
     return check_async();

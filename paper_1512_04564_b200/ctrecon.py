@@ -70,7 +70,7 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
            "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
-           "oslalm_zslab_solve"]
+           "oslalm_zslab_solve", "ct_sino_upload"]
 
 _lib = None
 
@@ -108,6 +108,7 @@ def load():
     L.oslalm_rho.argtypes = [ctypes.c_int64, ctypes.c_double]
     L.oslalm_rho.restype = ctypes.c_double
     L.ct_sync.argtypes = [vp]
+    L.ct_sino_upload.argtypes = [vp, vp, ct_views, vp, vp]
     L.ct_nccl_unique_id.argtypes = [P(ctypes.c_ubyte)]
     L.ct_dist_create.argtypes = [ctypes.c_int, ctypes.c_int, P(ctypes.c_ubyte), ctypes.c_int, P(vp)]
     L.ct_dist_destroy.argtypes = [vp]
@@ -118,7 +119,7 @@ def load():
                  "oslalm_workspace_size",
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
-                 "ct_sqs_diag_zslab", "oslalm_zslab_solve"):
+                 "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -265,6 +266,15 @@ def oslalm_state_h(geom, d_l, state, h_out, stream=None):
 
 def oslalm_rho(k, alpha):
     return load().oslalm_rho(int(k), float(alpha))
+
+
+def ct_sino_upload(geom, host, v, dev, stream=None):
+    """Copy views v of a (na, nt, ns) float32 host array (pinned) into the same rows of dev."""
+    if host.is_cuda or host.dtype != torch.float32 or not host.is_contiguous():
+        raise ValueError("host must be a contiguous float32 CPU tensor")
+    if host.shape != dev.shape:
+        raise ValueError("host and device sinograms differ in shape")
+    _check(load().ct_sino_upload(geom, ctypes.c_void_p(host.data_ptr()), v, _ptr(dev), _stream(stream)))
 
 
 def ct_sync(stream=None):

@@ -120,19 +120,44 @@ class HostPipeline:
         self.read = [torch.cuda.Event(), torch.cuda.Event()]   # snapshot i read back
         for e in self.used + self.read:
             e.record(self.comp)
+        self.sub_events = [None, None]
         self.i = 0
 
     def h2d_bytes(self, y_h, w_h):
         return y_h.numel() * y_h.element_size() + (w_h.numel() * w_h.element_size() if w_h is not None else 0)
 
-    def enqueue_copy_in(self, y_h, w_h):
-        """Queue the host->device copy of the next step's inputs (buffer i % 2)."""
+    def enqueue_copy_in(self, y_h, w_h, by_subset=False):
+        """Queue the host->device copy of the next step's inputs (buffer i % 2).
+        by_subset: copy subset by subset (ct_sino_upload) in the order the next
+        step visits them, with an event per subset, so that the step's first
+        sub-iterations start before the whole sinogram has arrived (used for
+        the first step, whose copy has no previous step to hide behind)."""
         b = self.i % 2
+        rec = self.rec
         with torch.cuda.stream(self.copy):
             self.copy.wait_event(self.used[b])
-            self.bufs[b][0].copy_(y_h, non_blocking=True)
-            if w_h is not None:
-                self.bufs[b][1].copy_(w_h, non_blocking=True)
+            if by_subset:
+                M = rec.params.M
+                na = rec.geom["na"]
+                k = rec.state.k
+                order = ([M - 1] if k == 0 else []) + [(k + q) % M for q in range(M)]
+                evs = {}
+                for m in order:
+                    if m in evs:
+                        continue
+                    v = C.views(m, M, (na - m + M - 1) // M)
+                    C.ct_sino_upload(rec.h, y_h, v, self.bufs[b][0], stream=self.copy)
+                    if w_h is not None:
+                        C.ct_sino_upload(rec.h, w_h, v, self.bufs[b][1], stream=self.copy)
+                    e = torch.cuda.Event()
+                    e.record(self.copy)
+                    evs[m] = e
+                self.sub_events[b] = evs
+            else:
+                self.bufs[b][0].copy_(y_h, non_blocking=True)
+                if w_h is not None:
+                    self.bufs[b][1].copy_(w_h, non_blocking=True)
+                self.sub_events[b] = None
             self.copied[b].record(self.copy)
 
     def step(self, n_subiters, x_h, next_inputs=None):
@@ -140,13 +165,27 @@ class HostPipeline:
         the copy of `next_inputs` = (y_h, w_h) for step i+1, read x back."""
         b = self.i % 2
         rec = self.rec
-        self.comp.wait_event(self.copied[b])
         rec.y, rec.w = self.bufs[b]
+        evs = self.sub_events[b]
+        if evs is None:
+            self.comp.wait_event(self.copied[b])
         if next_inputs is not None:
             self.i += 1
             self.enqueue_copy_in(*next_inputs)
             self.i -= 1
-        rec.run(n_subiters)
+        if evs is None:
+            rec.run(n_subiters)
+        else:
+            # sub-iteration by sub-iteration, each after its subset's copy (k = 0 also reads subset M-1)
+            M = rec.params.M
+            for _ in range(n_subiters):
+                k = rec.state.k
+                if k == 0:
+                    self.comp.wait_event(evs[M - 1])
+                self.comp.wait_event(evs[k % M])
+                rec.run(1)
+            self.comp.wait_event(self.copied[b])
+            self.sub_events[b] = None
         self.used[b].record(self.comp)
         self.comp.wait_event(self.read[b])
         self.snaps[b].copy_(rec.x)
