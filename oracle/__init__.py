@@ -15,7 +15,11 @@ Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s cpu_baseline /
 `--impl reference` legs may import this package.  It shares no code with
 `paper_1512_04564_b200/` and never imports it.
 
-Parity status per function is listed in DESIGN.md "Oracle pins"; Algorithm 1
-with M > 1 on the BASELINE configs is "parity unpinned" beyond the pins of its
-parts (P9 in SURVEY.md 8c.4): no external value exists for it.
+Parity status per function is listed in DESIGN.md "Oracle pins".  Algorithm 1
+with M > 1 (P9 in SURVEY.md 8c.4) is pinned by reduction: on a scan whose
+subsets are exact copies of each other (M pitch-0 turns) the ordered-subsets
+gradient is exact and the M-subset iterates must equal the M = 1 iterates,
+which are pinned to the literal Eq. 25 and to the dense PWLS minimiser
+(tests/test_oracle_alg.py P7, P9).  No external value exists for M > 1 on
+the BASELINE configs themselves.
 """

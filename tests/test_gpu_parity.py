@@ -404,6 +404,30 @@ def test_deterministic_repeat(C):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("kind,V0,M", [("fan2d_arc", 8, 3), ("axial_flat", 5, 3)])
+def test_exact_subsets_gpu_M_equals_M1(C, kind, V0, M):
+    """P9 on the GPU: with subsets that are exact copies of each other (M
+    pitch-0 turns, tests/test_oracle_alg.py), relaxed OS-LALM with M subsets
+    equals the M = 1 run sub-iteration for sub-iteration, and both match the
+    oracle."""
+    from tests.test_oracle_alg import repeated_turn_problem
+    prob, x0 = repeated_turn_problem(kind, V0, M)
+    g = prob.g
+    reg = dict(potential="hyperbola", delta=0.01, betas=[5.0] * (13 if g["dim"] == 3 else 4),
+               n_dirs=13 if g["dim"] == 3 else 4)
+    DL = prob.D_L()
+    xs = []
+    for mm, iters in ((M, 2), (1, 2 * M)):
+        pb = dict(geom=g, y=prob.y, w=prob.w, x0=x0, reg=reg, solver=dict(M=mm, alpha=1.999))
+        rec = _gpu_recon(pb)
+        rec.run(mm * iters)
+        xs.append(host(rec.x))
+        rec.close()
+    xo, _, _ = alg.alg1(prob, x0, M, 1.999, 2, DL=DL)
+    assert rel(xs[0], xs[1]) <= 1e-5, rel(xs[0], xs[1])
+    assert rel(xs[0], xo) <= 1e-4, rel(xs[0], xo)
+
+
 def test_sino_upload_and_host_pipeline(C):
     """ct_sino_upload copies exactly the rows of the given views; the host
     pipeline (first step subset by subset, then double-buffered whole copies)

@@ -1,7 +1,7 @@
 """Pins of the oracle iteration — CPU only.
 
 Algorithm 1 has no external value to compare with for
-M > 1 (P9 "parity unpinned"); its parts are pinned here:
+M > 1 on the BASELINE configs; its parts are pinned here:
   P7a  Alg. 1 with M = 1 equals the literal Eq. 25 iteration with an explicit
        G^{1/2}, nu stays 0, for
        alpha in {1, 1.5, 1.999}, fixed rho and Eq. 37;
@@ -9,7 +9,12 @@ M > 1 (P9 "parity unpinned"); its parts are pinned here:
   P7c  quadratic potential, M = 1: Alg. 1 converges to the dense PWLS
        minimiser (A'WA + H_R)^{-1}A'Wy; alpha = 1.999 gets there in fewer
        iterations than alpha = 1 (Theorem 2, PAPER.md:263);
-  P8   Eq. 37 values, subset partition, work accounting, feasibility.
+  P8   Eq. 37 values, subset partition, work accounting, feasibility;
+  P9   M > 1: on a scan whose subsets are exact copies of each other (M turns,
+       pitch 0) the ordered-subsets gradient is exact, and Alg. 1 / Alg. 2
+       with M subsets equal the M = 1 iterations sub-iteration by
+       sub-iteration (the subset loop, the M scaling, the rho counting and
+       the line-1 subset are all exercised).
 """
 import math
 
@@ -189,3 +194,65 @@ def test_os_sqs_monotone_descent_and_alg2_rho1_is_os_sqs():
         assert np.linalg.norm(x2 - xs) <= 1e-12 * np.linalg.norm(xs), alpha
     # a different visiting order gives different iterates (the pin is not vacuous)
     assert np.linalg.norm(alg.os_sqs(prob, x0, M, iters, DL=DL) - xs) > 1e-8 * np.linalg.norm(xs)
+
+
+# ------------------------------------------------------------------ P9 (M > 1)
+def repeated_turn_problem(kind, V0, M, seed=3):
+    """A pitch-0 scan of M full turns with V0 views per turn (na = M V0,
+    gcd(M, V0) = 1): view v sits at angle 360 v / V0, so the views of every
+    subset m = {v = m mod M} (PAPER.md:441-442 ordering, R4) are the V0
+    distinct angles once each (subset partition R4), and the data of a view
+    depend on its angle only.  Then M grad L_m(x) = grad L(x) exactly for every
+    m: the ordered-subsets approximation of line 6 is exact, and Algorithm 1
+    with M subsets must coincide, sub-iteration by sub-iteration, with
+    Algorithm 1 with M = 1 on the same data (rho_k counts sub-iterations, R2;
+    line 1 uses M grad L_{M-1} = grad L, R1)."""
+    assert math.gcd(M, V0) == 1
+    g = tiny(kind, na=M * V0, orbit_deg=360.0 * M, pitch=0.0)
+    rng = np.random.default_rng(seed)
+    shape = P.vol_shape(g)
+    xt = 0.02 + 0.01 * rng.random(shape)
+    ell = P.forward(g, xt)
+    one = ell[:V0]                        # one turn; later turns repeat its angles
+    I0 = 1e4
+    c = np.maximum(rng.poisson(I0 * np.exp(-one)).astype(np.float64), 1.0)
+    y = np.concatenate([np.log(I0 / c)] * M)
+    w = np.concatenate([c / I0 * 10.0] * M)
+    n_dirs = 13 if g["dim"] == 3 else 4
+    prob = alg.Problem(g, y, w, "hyperbola", 0.01, [5.0] * n_dirs, n_dirs)
+    x0 = np.clip(xt + 0.005 * rng.standard_normal(shape), 0, None)
+    return prob, x0
+
+
+@pytest.mark.parametrize("kind,V0,M", [("fan2d_arc", 8, 3), ("fan2d_flat", 7, 4), ("axial_flat", 5, 3)])
+def test_os_with_exact_subsets_reduces_to_M1(kind, V0, M):
+    prob, x0 = repeated_turn_problem(kind, V0, M)
+    # the premise: every subset's scaled gradient is the full gradient
+    gf = prob.grad_L(x0)
+    for m in range(M):
+        assert np.max(np.abs(M * prob.grad_L_subset(x0, m, M) - gf)) <= 1e-9 * np.max(np.abs(gf))
+    DL = prob.D_L()
+    K = 3
+    for alpha in (1.0, 1.999):
+        tr_M, tr_1 = {}, {}
+        alg.alg1(prob, x0, M, alpha, K, DL=DL, trace=tr_M)
+        alg.alg1(prob, x0, 1, alpha, K * M, DL=DL, trace=tr_1)
+        for k in range(1, K * M + 1):
+            for a, b in zip(tr_M[k], tr_1[k]):
+                assert np.max(np.abs(a - b)) <= 1e-9 * max(np.max(np.abs(b)), 1e-30), (alpha, k)
+    x_M, g_M = alg.alg2(prob, x0, M, 1.5, K, DL=DL)
+    x_1, g_1 = alg.alg2(prob, x0, 1, 1.5, K * M, DL=DL)
+    assert np.max(np.abs(x_M - x_1)) <= 1e-9 * np.max(np.abs(x_1))
+    assert np.max(np.abs(g_M - g_1)) <= 1e-9 * np.max(np.abs(g_1))
+
+
+def test_os_reduction_has_teeth():
+    """On an ordinary one-turn scan the subsets differ, and the same comparison
+    fails by orders of magnitude more than its tolerance."""
+    prob, x0, _ = tiny_problem("fan2d_arc")
+    DL = prob.D_L()
+    tr_M, tr_1 = {}, {}
+    alg.alg1(prob, x0, 3, 1.999, 1, DL=DL, trace=tr_M)
+    alg.alg1(prob, x0, 1, 1.999, 3, DL=DL, trace=tr_1)
+    d = np.max(np.abs(tr_M[3][0] - tr_1[3][0])) / np.max(np.abs(tr_1[3][0]))
+    assert d > 1e-5, d
