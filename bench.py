@@ -325,7 +325,7 @@ def run_cuda(args):
         x_h = [torch.empty(rec.x.shape, dtype=torch.float32).pin_memory() for _ in range(2)]
         pipe = HostPipeline(rec)
         # untimed: one cycle over both device buffers (captures the solve graph of each)
-        pipe.enqueue_copy_in(y_h, w_h, by_subset=True)
+        pipe.enqueue_copy_in(y_h, w_h, by_subset=pipe.h2d_bytes(y_h, w_h) >= (256 << 20))
         pipe.step(M, x_h[0], next_inputs=(y_h, w_h))
         pipe.step(M, x_h[1], next_inputs=None)
         pipe.finish()
@@ -333,7 +333,10 @@ def run_cuda(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        pipe.enqueue_copy_in(y_h, w_h, by_subset=True)   # first step: subset by subset (nothing to hide behind)
+        # first step: subset by subset (nothing to hide behind) when the copy is long enough to matter;
+        # small sinograms take one copy (per-subset calls would cost more host time than they hide)
+        split = pipe.h2d_bytes(y_h, w_h) >= (256 << 20)
+        pipe.enqueue_copy_in(y_h, w_h, by_subset=split)
         for it in range(args.steps):
             nxt = (y_h, w_h) if it + 1 < args.steps else None
             pipe.step(M, x_h[it % 2], next_inputs=nxt)
@@ -345,7 +348,7 @@ def run_cuda(args):
                "h2d_bytes_per_step": int(pipe.h2d_bytes(y_h, w_h)),
                "d2h_bytes_per_step": int(x_h[0].numel() * 4),
                "pipelined": "host->device copy of step i+1 and read-back of step i overlap step i+1's solve; "
-                            "the first step's copy goes subset by subset ahead of its sub-iterations"}
+                            "the first step's copy goes subset by subset ahead of its sub-iterations (sinograms >= 256 MiB)"}
 
     if rank != 0:
         if world > 1:
