@@ -343,6 +343,17 @@ static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, V
         }
         return;
     }
+    // fewer than ~16 blocks per SM: two threads per pixel (the last partial wave otherwise idles SMs)
+    if ((long long)grid.x * grid.y < 148LL * 16) {
+        dim3 block(32, BK_Y, 2);
+        switch (epi) {
+            case BK_WRITE: k_back2<ARC, BK_WRITE, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_ACCUM: k_back2<ARC, BK_ACCUM, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_INIT: k_back2<ARC, BK_INIT, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            default: k_back2<ARC, BK_UPDATE, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        }
+        return;
+    }
     dim3 block(32, BK_Y, 1);
     switch (epi) {
         case BK_WRITE: k_back2<ARC, BK_WRITE, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
