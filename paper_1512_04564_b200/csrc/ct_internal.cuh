@@ -86,6 +86,12 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// 1/x in one MUFU.RCP (no denormal-divisor fix-up: callers pass x > 0 well above 2^-126)
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // L2 evict-last policy for data re-read by many views (the forward's z-prefix
 // array) and a gather that carries it; streaming (evict-first) for data read

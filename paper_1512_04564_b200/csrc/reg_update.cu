@@ -192,12 +192,16 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     // Interior columns load the 3x3 block unconditionally from a clamped plane (a
     // plane outside the volume is never weighted: the stencil checks km/kp there).
     const int klo = A.halo_lo ? -1 : 0, khi = A.halo_hi ? G.nz : G.nz - 1;   // readable planes of x
+    const float* __restrict__ xlo = x + (long long)klo * (long long)nxy;       // plane klo (kappa: klo = 0)
     auto load_plane = [&](auto slot_c, int k) {
         constexpr int S = decltype(slot_c)::value;
         if (inxy) {
+            // interior column: a 32-bit offset from the lowest readable plane klo (the halo plane
+            // -1 of a z-slab lies below x); (kc - klo) * nxy + col - nx - 1 < 2^32
             const int kc = min(max(k, klo), khi);
-            const float* __restrict__ p = x + ((long long)kc * nxy + col - nx - 1u);
-            const float* __restrict__ pk = KAPPA ? kappa + ((long long)kc * nxy + col - nx - 1u) : nullptr;
+            const unsigned off = (unsigned)(kc - klo) * nxy + col - nx - 1u;
+            const float* __restrict__ p = xlo + off;
+            const float* __restrict__ pk = KAPPA ? kappa + off : nullptr;
 #pragma unroll
             for (int dy = 0; dy < 3; dy++) {
 #pragma unroll
@@ -265,7 +269,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
                 const float s = fmaf(rho, htv, (1.f - rho) * Gv[Q]);
                 const float den = fmaf(rho, d, 2.f * cs);
                 xnew = xv;
-                if (den > 0.f) xnew = fminf(fmaxf(xv - __fdividef(fmaf(del, gs, s), den), A.box_lo), A.box_hi);
+                if (den > 0.f) xnew = fminf(fmaxf(xv - fmaf(del, gs, s) * rcp_ftz(den), A.box_lo), A.box_hi);
                 xn[idx] = xnew;
                 if (!simple) A.ht[idx] = (1.f - alpha) * fmaf(d, xnew - xv, htv);
             } else {
