@@ -286,6 +286,14 @@ ct_status oslalm_profile(const ct_geom* g, const float* y, const float* w, const
  * The projector's algorithmic FLOP count is 2 per nonzero. */
 ct_status ct_count_nnz(const ct_geom* g, ct_views v, uint64_t* d_count, ct_stream s);
 
+/* The units of SURVEY.md §8d's algorithmic FLOP figure for the projector pair on
+ * views v: d_counts (device uint64[3]) += {nnz(A_v), in-cone voxel-view pairs
+ * (voxels with at least one nonzero in the view), in-cone column-view pairs
+ * (voxel columns with at least one nonzero in the view)}.  The bench's FLOP
+ * count per projection is 2 nnz + 6 pairs + 150 columns (MACs, axial setup per
+ * voxel, transaxial setup per column).  Errors as ct_count_nnz. */
+ct_status ct_count_work(const ct_geom* g, ct_views v, uint64_t* d_counts, ct_stream s);
+
 /* h = D_L x - htilde (Algorithm 1's h, for checkpoints and parity checks). */
 ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out, ct_stream s);
 

@@ -677,6 +677,15 @@ extern "C" ct_status ct_count_nnz(const ct_geom* g, ct_views v, uint64_t* d_coun
     return check_async();
 }
 
+extern "C" ct_status ct_count_work(const ct_geom* g, ct_views v, uint64_t* d_counts, ct_stream s) {
+    if (!g || !d_counts) return fail(CT_E_CONFIG, "ct_count_work: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    DeviceGuard guard(g->device);
+    launch_count_work(g->G, g->vtab, to_views(v), (unsigned long long*)d_counts, (cudaStream_t)s);
+    return check_async();
+}
+
 extern "C" ct_status oslalm_state_h(const ct_geom* g, const float* d_l, const oslalm_state* st, float* h_out,
                                     ct_stream s) {
     if (!g || !d_l || !st || !st->x || !st->htilde || !h_out) return fail(CT_E_CONFIG, "oslalm_state_h: NULL argument");

@@ -71,6 +71,8 @@ void launch_check(const DGeom& G, const float* x, const float* xref, int* flag, 
 
 // nonzero entries of A on views v, added into *count (device)
 void launch_count(const DGeom& G, const float4* vtab, Views v, unsigned long long* count, cudaStream_t s);
+// count3[0] += nnz, count3[1] += in-cone voxel-view pairs, count3[2] += in-cone column-view pairs
+void launch_count_work(const DGeom& G, const float4* vtab, Views v, unsigned long long* count3, cudaStream_t s);
 
 int64_t launches_add(int64_t n);  // launch accounting
 

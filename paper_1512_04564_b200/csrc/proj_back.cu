@@ -404,12 +404,15 @@ void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, co
 // ((v,t,s),(i,j,k)) is nonzero iff F1(s) > 0 and F2(k,t) > 0.
 namespace ctr {
 
-template <bool ARC, int DIM>
+// WORK: also count[1] += in-cone voxel-view pairs (voxels with a nonzero in the
+// view) and count[2] += column-view pairs with a nonzero -- the units of SURVEY
+// §8d's algorithmic FLOP figure.
+template <bool ARC, int DIM, bool WORK>
 __global__ void __launch_bounds__(128) k_count(DGeom G, const float4* __restrict__ vtab, Views V,
                                                unsigned long long* __restrict__ count) {
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * 4 + threadIdx.y;
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, pvox = 0, pcol = 0;
     if (i < G.nx && j < G.ny) {
         for (int vi = 0; vi < V.count; vi++) {
             const float4 vw = __ldg(&vtab[V.start + vi * V.stride]);
@@ -420,31 +423,58 @@ __global__ void __launch_bounds__(128) k_count(DGeom G, const float4* __restrict
             int ncz = 0;
             for (int s = slo; s <= shi; s++) ncz += sf_F1(f, s) > 0.f;
             if (ncz == 0) continue;
-            long long rows = 1;
+            long long rows = 1, vin = 1;
             if (DIM == 3) {
                 rows = 0;
+                vin = 0;
                 for (int k = 0; k < G.nz; k++) {
                     const float lo = fmaxf(voxel_b(f, k), 0.f), hi = fminf(voxel_b(f, k + 1), (float)G.nt);
-                    if (hi > lo) rows += (long long)ceilf(hi) - (long long)floorf(lo);
+                    if (hi > lo) {
+                        rows += (long long)ceilf(hi) - (long long)floorf(lo);
+                        vin++;
+                    }
                 }
             }
             acc += (unsigned long long)ncz * (unsigned long long)rows;
+            if (WORK && vin > 0) {
+                pvox += (unsigned long long)vin;
+                pcol++;
+            }
         }
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(count, acc);
+    for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (WORK) {
+            pvox += __shfl_down_sync(0xffffffffu, pvox, o);
+            pcol += __shfl_down_sync(0xffffffffu, pcol, o);
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (acc) atomicAdd(count, acc);
+        if (WORK && pvox) atomicAdd(count + 1, pvox);
+        if (WORK && pcol) atomicAdd(count + 2, pcol);
+    }
+}
+
+template <bool WORK>
+static void count_launch(const DGeom& G, const float4* vtab, Views v, unsigned long long* count, cudaStream_t s) {
+    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4);
+    if (G.arc) {
+        if (G.dim == 3) k_count<true, 3, WORK><<<grid, block, 0, s>>>(G, vtab, v, count);
+        else k_count<true, 2, WORK><<<grid, block, 0, s>>>(G, vtab, v, count);
+    } else {
+        if (G.dim == 3) k_count<false, 3, WORK><<<grid, block, 0, s>>>(G, vtab, v, count);
+        else k_count<false, 2, WORK><<<grid, block, 0, s>>>(G, vtab, v, count);
+    }
+    launches_add(1);
 }
 
 void launch_count(const DGeom& G, const float4* vtab, Views v, unsigned long long* count, cudaStream_t s) {
-    dim3 block(32, 4), grid((G.nx + 31) / 32, (G.ny + 3) / 4);
-    if (G.arc) {
-        if (G.dim == 3) k_count<true, 3><<<grid, block, 0, s>>>(G, vtab, v, count);
-        else k_count<true, 2><<<grid, block, 0, s>>>(G, vtab, v, count);
-    } else {
-        if (G.dim == 3) k_count<false, 3><<<grid, block, 0, s>>>(G, vtab, v, count);
-        else k_count<false, 2><<<grid, block, 0, s>>>(G, vtab, v, count);
-    }
-    launches_add(1);
+    count_launch<false>(G, vtab, v, count, s);
+}
+
+void launch_count_work(const DGeom& G, const float4* vtab, Views v, unsigned long long* count3, cudaStream_t s) {
+    count_launch<true>(G, vtab, v, count3, s);
 }
 
 }  // namespace ctr

@@ -70,7 +70,7 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
            "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
-           "oslalm_zslab_solve", "ct_sino_upload"]
+           "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work"]
 
 _lib = None
 
@@ -105,6 +105,7 @@ def load():
     L.oslalm_profile.argtypes = [vp, vp, vp, P(ct_reg_desc), vp, vp, P(oslalm_params), P(oslalm_state),
                                  ctypes.c_int, vp, vp, ctypes.c_size_t, vp, P(ctypes.c_double)]
     L.ct_count_nnz.argtypes = [vp, ct_views, vp, vp]
+    L.ct_count_work.argtypes = [vp, ct_views, vp, vp]
     L.oslalm_rho.argtypes = [ctypes.c_int64, ctypes.c_double]
     L.oslalm_rho.restype = ctypes.c_double
     L.ct_sync.argtypes = [vp]
@@ -119,7 +120,7 @@ def load():
                  "oslalm_workspace_size",
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
-                 "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload"):
+                 "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -258,6 +259,13 @@ def ct_count_nnz(geom, v, stream=None):
     cnt = torch.zeros(1, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
     _check(load().ct_count_nnz(geom, v, ctypes.c_void_p(cnt.data_ptr()), _stream(stream)))
     return int(cnt.item())
+
+
+def ct_count_work(geom, v, stream=None):
+    """(nnz, in-cone voxel-view pairs, in-cone column-view pairs) of A on views v."""
+    cnt = torch.zeros(3, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
+    _check(load().ct_count_work(geom, v, ctypes.c_void_p(cnt.data_ptr()), _stream(stream)))
+    return tuple(int(c) for c in cnt.tolist())
 
 
 def oslalm_state_h(geom, d_l, state, h_out, stream=None):

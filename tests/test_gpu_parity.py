@@ -404,6 +404,47 @@ def test_deterministic_repeat(C):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("kind", ["axial_flat", "helical_arc", "fan2d_flat"])
+def test_count_work_matches_dense_oracle_matrix(C, kind):
+    """ct_count_work / ct_count_nnz (the units of the bench's algorithmic FLOP figure)
+    against the oracle's dense A built column by column: nonzeros, in-cone
+    voxel-view pairs and column-view pairs (float32 vs float64 footprint edges
+    may flip a handful of entries)."""
+    g = tiny(kind)
+    shape = P.vol_shape(g)
+    nv = int(np.prod(shape))
+    na = g["na"]
+    cols = []
+    nth = P.max_threads()
+    P.set_threads(1)            # ~1000 tiny calls: thread start-up would dominate
+    try:
+        for q in range(nv):
+            e = np.zeros(nv)
+            e[q] = 1.0
+            cols.append(P.forward(g, e.reshape(shape)).reshape(na, -1))   # (views, rays of a view)
+    finally:
+        P.set_threads(nth)
+    A = np.stack(cols, axis=-1) > 0                                 # (views, rays, voxels)
+    nnz = int(A.sum())
+    hit = A.any(axis=1)                                             # (views, voxels)
+    pvox = int(hit.sum())
+    pcol = int(hit.reshape(na, shape[0], -1).any(axis=1).sum())
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        a, b, c = C.ct_count_work(h, C.views(0, 1, na))
+        assert a == C.ct_count_nnz(h, C.views(0, 1, na))
+        assert abs(a - nnz) <= 2e-3 * nnz, (a, nnz)
+        assert abs(b - pvox) <= 2e-3 * pvox, (b, pvox)
+        assert abs(c - pcol) <= 2e-3 * pcol, (c, pcol)
+        if g["dim"] == 2:
+            assert b == c
+        # additive over view subsets
+        parts = [C.ct_count_work(h, C.views(m, 3, (na - m + 2) // 3)) for m in range(3)]
+        assert tuple(sum(p[i] for p in parts) for i in range(3)) == (a, b, c)
+    finally:
+        C.ct_geom_destroy(h)
+
+
 @pytest.mark.parametrize("kind,V0,M", [("fan2d_arc", 8, 3), ("axial_flat", 5, 3)])
 def test_exact_subsets_gpu_M_equals_M1(C, kind, V0, M):
     """P9 on the GPU: with subsets that are exact copies of each other (M
