@@ -300,6 +300,20 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         fp_axial<ARC>(G, fb, zs, f.B0, f.H);
                         cand = f.B0 < (float)G.nt && fmaf(fnz, f.H, f.B0) > 0.f;
                     }
+                    // PFX: the top-boundary gather (lane 31's upper row edge) is issued before the
+                    // transaxial footprint so that its latency overlaps that arithmetic
+                    float invH = 0.f, b0 = 0.f, ft = 0.f;
+                    float2 qt = make_float2(0.f, 0.f);
+                    if (PFX && cand) {
+                        invH = __fdividef(1.f, f.H);
+                        // f' = (u - B0)/H - 1/2 (voxel coordinate minus 1/2); X at the top
+                        // boundary RPL*32 of the lanes' rows (lane 31 needs it)
+                        b0 = fmaf(-f.B0, invH, -0.5f);
+                        const float2* __restrict__ Qc = Q + (unsigned)(j * G.nx + i) * (unsigned)pfx_stride;
+                        ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), -0.5f), fnz - 0.5f);
+                        const float rt = __fadd_rn(ft, 12582912.0f);
+                        qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
+                    }
                     if (cand) {
                         fp_trans<ARC>(G, cb, sb, fb, f);
                         // F1 of the 4 detector columns from 5 edge evaluations
@@ -316,17 +330,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             const float Ls = PFX ? f.lxy * f.H : f.lxy;
                             eL = make_float4(Ls * Fc[0], Ls * Fc[1], Ls * Fc[2], Ls * Fc[3]);
                             if (PFX) {
-                                const float invH = __fdividef(1.f, f.H);
-                                // f' = (u - B0)/H - 1/2 (voxel coordinate minus 1/2); X at the top
-                                // boundary RPL*32 of the lanes' rows (lane 31 needs it)
-                                const float b0 = fmaf(-f.B0, invH, -0.5f);
-                                const float2* __restrict__ Qc =
-                                    Q + (unsigned)(j * G.nx + i) * (unsigned)pfx_stride;
-                                const float ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), -0.5f), fnz - 0.5f);
-                                const float rt = __fadd_rn(ft, 12582912.0f);
-                                const float2 qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
-                                const float xtop = fmaf(ft, qt.y, qt.x);
-                                eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), xtop);
+                                eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), fmaf(ft, qt.y, qt.x));
                             } else {
                                 eG = make_float4(f.B0, f.H, __int_as_float(j * G.nx + i), 0.f);
                             }
