@@ -196,6 +196,9 @@ constexpr int F3_CPW = 4;
 constexpr int F3_BS = 32 * F3_WARPS;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
+#ifndef F3_PREYW
+#define F3_PREYW 1     // epilogue y, w copied into shared memory by cp.async at kernel start
+#endif
 #ifndef F3_MINB
 #define F3_MINB 8  // 64 registers: 8 blocks of 4 warps per SM to hide the prefix-gather latency
 #endif
@@ -207,6 +210,10 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     __shared__ float4 qL[F3_WARPS][32];    // L for the 4 detector columns
     __shared__ float4 qG[F3_WARPS][32];    // PFX: (-B0/H, 1/H, col, -) ; direct: (B0, H, col, -)
     __shared__ float stage[32 * RPL][F3_CPB + 1];
+#if F3_PREYW
+    __shared__ float ysm[MODE == FWD_RESID ? 32 * RPL : 1][F3_CPB];   // epilogue operands (cp.async)
+    __shared__ float wsm[MODE != FWD_PLAIN ? 32 * RPL : 1][F3_CPB];
+#endif
     constexpr bool ONES = (MODE == FWD_ONES_W);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const Views V = select_views(ctl, vsel);
@@ -228,6 +235,31 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
         for (int r = 0; r < RPL; r++) acc[c][r] = 0.f;
+
+#if F3_PREYW
+    // y and w of the block's (row, column) outputs are read only by the epilogue: start their
+    // copies into shared memory now (cp.async) so that the epilogue does not wait on HBM
+    constexpr bool YW = (MODE != FWD_PLAIN);
+    if (YW) {
+        for (int q = threadIdx.x; q < G.nt * F3_CPB; q += F3_BS) {
+            const int t = q / F3_CPB, c = q % F3_CPB;
+            const int ss = sb0 + c;
+            if (ss >= G.ns) continue;
+            const size_t a = ((size_t)v * G.nt + t) * G.ns + ss;
+            if (MODE == FWD_RESID)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(&ysm[t][c])),
+                             "l"(__cvta_generic_to_global(y + a))
+                             : "memory");
+            if (w)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                 (unsigned)__cvta_generic_to_shared(&wsm[t][c])),
+                             "l"(__cvta_generic_to_global(w + a))
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+#endif
 
     if (s0 < G.ns) {  // warp-uniform
         const int s3 = min(s0 + F3_CPW - 1, G.ns - 1);
@@ -413,6 +445,9 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
         for (int r = 0; r < RPL; r++) stage[RPL * lane + r][wid * F3_CPW + c] = acc[c][r];
+#if F3_PREYW
+    if (YW) asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
     __syncthreads();
     for (int q = threadIdx.x; q < G.nt * F3_CPB; q += F3_BS) {
         const int t = q / F3_CPB, c = q % F3_CPB;
@@ -424,11 +459,17 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         if (MODE == FWD_PLAIN) {
             out[o] = p;
         } else {
+#if F3_PREYW
+            const float wv = w ? wsm[t][c] : 1.f;
+            if (MODE == FWD_RESID) out[o] = lz * wv * (p - ysm[t][c]);
+            else out[o] = lz * wv * p;
+#else
             // y, w are read once per sub-iteration: streaming (evict-first) loads
             const size_t a = ((size_t)v * G.nt + t) * G.ns + ss;
             const float wv = w ? __ldcs(&w[a]) : 1.f;
             if (MODE == FWD_RESID) out[o] = lz * wv * (p - __ldcs(&y[a]));
             else out[o] = lz * wv * p;
+#endif
         }
     }
 }
