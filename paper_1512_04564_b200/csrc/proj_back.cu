@@ -139,6 +139,9 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
 //      (one 8-byte shared load and one FFMA per voxel boundary, magic-number
 //      rounding).
 template <bool ARC, int EPI, bool LZ, int BK_KZ>
+#ifndef BK_EPB
+#define BK_EPB 12      // voxels per batch of the g/htilde epilogue (loads of a batch issued together)
+#endif
 #ifndef BK_RM24
 #define BK_RM24 40     // rows buffered per pass at KZ = 24 (41 x 128 float2 = 42 KB)
 #endif
@@ -277,29 +280,51 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     }
 
     // epilogue
-    float rho = 0.f, alpha = 0.f;
-    if (EPI == BK_UPDATE) {
-        rho = rho_of_k(ctl);
-        alpha = ctl->alpha;
-    }
     const int kz = min(BK_KZ, G.nz - k0);
+    if (EPI == BK_UPDATE) {
+        // lines 7-8: g and htilde of the chunk in batches of EB voxels, every load of a batch
+        // issued before its first use (one HBM round trip per batch instead of per voxel)
+        const float rho = rho_of_k(ctl), alpha = ctl->alpha;
+        const bool simple = ctl->simple;
+        const float inv = 1.f / (rho + 1.f), ri = rho * inv, oma = 1.f - alpha;
+        const size_t base = (size_t)k0 * G.nxy + (size_t)j * G.nx + i;
+        constexpr int EB = (BK_KZ % BK_EPB == 0) ? BK_EPB : 8;
 #pragma unroll
-    for (int q = 0; q < BK_KZ; q++) {
-        if (q < kz) {
-            const size_t idx = (size_t)(k0 + q) * G.nxy + (size_t)j * G.nx + i;
-            const float z = scale * acc[q];
-            if (EPI == BK_WRITE) {
-                out[idx] = z;
-            } else if (EPI == BK_ACCUM) {
-                out[idx] += z;
-            } else if (EPI == BK_INIT) {
-                gbuf[idx] = z;
-                htbuf[idx] = z;
-            } else {
-                const float gv = gbuf[idx];
-                const float inv = 1.f / (rho + 1.f);
-                gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
-                htbuf[idx] = ctl->simple ? z : fmaf(alpha, z, htbuf[idx]);
+        for (int b = 0; b < BK_KZ; b += EB) {
+            float gv[EB], hv[EB];
+#pragma unroll
+            for (int q = 0; q < EB; q++) {
+                gv[q] = hv[q] = 0.f;
+                if (b + q < kz) {
+                    const size_t idx = base + (size_t)(b + q) * G.nxy;
+                    gv[q] = gbuf[idx];
+                    if (!simple) hv[q] = htbuf[idx];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < EB; q++) {
+                if (b + q < kz) {
+                    const size_t idx = base + (size_t)(b + q) * G.nxy;
+                    const float z = scale * acc[b + q];
+                    gbuf[idx] = fmaf(ri, fmaf(alpha, z, oma * gv[q]), gv[q] * inv);
+                    htbuf[idx] = simple ? z : fmaf(alpha, z, hv[q]);
+                }
+            }
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < BK_KZ; q++) {
+            if (q < kz) {
+                const size_t idx = (size_t)(k0 + q) * G.nxy + (size_t)j * G.nx + i;
+                const float z = scale * acc[q];
+                if (EPI == BK_WRITE) {
+                    out[idx] = z;
+                } else if (EPI == BK_ACCUM) {
+                    out[idx] += z;
+                } else {
+                    gbuf[idx] = z;
+                    htbuf[idx] = z;
+                }
             }
         }
     }
