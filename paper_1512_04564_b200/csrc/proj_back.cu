@@ -139,6 +139,9 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
 //      (one 8-byte shared load and one FFMA per voxel boundary, magic-number
 //      rounding).
 template <bool ARC, int EPI, bool LZ, int BK_KZ>
+#ifndef BK_VSM
+#define BK_VSM 128     // view descriptors of the block's window staged in shared memory
+#endif
 #ifndef BK_EPB
 #define BK_EPB 12      // voxels per batch of the g/htilde epilogue (loads of a batch issued together)
 #endif
@@ -158,15 +161,9 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
     const int k0 = blockIdx.z * BK_KZ;
-    if (i >= G.nx || j >= G.ny) return;
     const Views V = select_views(ctl, vsel);
     const int nt = G.nt;
     const float fkz = (float)min(BK_KZ, G.nz - k0);
-    float2* __restrict__ cs = &csb[0][tid];
-
-    float acc[BK_KZ];
-#pragma unroll
-    for (int q = 0; q < BK_KZ; q++) acc[q] = 0.f;
 
     // Helical view window of the block's z-chunk: the chunk [zlo, zhi] can reach the
     // detector rows [0, nt) only if zlo - (nt - tc)/m < z_s < zhi + tc/m for some
@@ -187,10 +184,21 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         vi0 = max(vi0, (int)floorf(ia) - 1);
         vi1 = min(vi1, (int)ceilf(ib) + 2);
     }
+    // the window's view descriptors in shared memory (the per-view set-up otherwise waits on a
+    // global load the row gathers have evicted from L1); views past BK_VSM are read directly
+    __shared__ float4 vsm[BK_VSM];
+    const int nstage = max(0, min(vi1 - vi0, BK_VSM));
+    for (int q = tid; q < nstage; q += BK_BS) vsm[q] = __ldg(&vtab[V.start + (vi0 + q) * V.stride]);
+    __syncthreads();
+    if (i >= G.nx || j >= G.ny) return;
+    float2* __restrict__ cs = &csb[0][tid];
+
+    float acc[BK_KZ];
+#pragma unroll
+    for (int q = 0; q < BK_KZ; q++) acc[q] = 0.f;
 
     for (int vi = vi0; vi < vi1; vi++) {
-        const int v = V.start + vi * V.stride;
-        const float4 vw = __ldg(&vtab[v]);
+        const float4 vw = vi - vi0 < BK_VSM ? vsm[vi - vi0] : __ldg(&vtab[V.start + vi * V.stride]);
         FpBase fb;
         fp_base(G, vw.x, vw.y, i, j, fb);
         float B0, H;
