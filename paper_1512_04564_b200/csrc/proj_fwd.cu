@@ -193,7 +193,6 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #endif
 constexpr int F3_WARPS = F3_NWARPS;
 constexpr int F3_CPW = 4;
-constexpr int F3_BS = 32 * F3_WARPS;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
 #ifndef F3_PREYW
@@ -202,17 +201,19 @@ constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 #ifndef F3_MINB
 #define F3_MINB 8  // 64 registers: 8 blocks of 4 warps per SM to hide the prefix-gather latency
 #endif
-template <bool ARC, int MODE, int RPL, bool PFX>
-__global__ void __launch_bounds__(F3_BS, F3_MINB)
+// NW warps per block (4, or 2 for small grids: finer blocks shorten the last wave); 32 / NW
+// blocks per SM keep the same 32 resident warps at 64 registers
+template <bool ARC, int MODE, int RPL, bool PFX, int NW>
+__global__ void __launch_bounds__(32 * NW, F3_MINB * F3_NWARPS / NW)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
-    __shared__ float4 qL[F3_WARPS][32];    // L for the 4 detector columns
-    __shared__ float4 qG[F3_WARPS][32];    // PFX: (-B0/H, 1/H, col, -) ; direct: (B0, H, col, -)
-    __shared__ float stage[32 * RPL][F3_CPB + 1];
+    __shared__ float4 qL[NW][32];    // L for the 4 detector columns
+    __shared__ float4 qG[NW][32];    // PFX: (-B0/H, 1/H, col, -) ; direct: (B0, H, col, -)
+    __shared__ float stage[32 * RPL][(NW * F3_CPW) + 1];
 #if F3_PREYW
-    __shared__ float ysm[MODE == FWD_RESID ? 32 * RPL : 1][F3_CPB];   // epilogue operands (cp.async)
-    __shared__ float wsm[MODE != FWD_PLAIN ? 32 * RPL : 1][F3_CPB];
+    __shared__ float ysm[MODE == FWD_RESID ? 32 * RPL : 1][(NW * F3_CPW)];   // epilogue operands (cp.async)
+    __shared__ float wsm[MODE != FWD_PLAIN ? 32 * RPL : 1][(NW * F3_CPW)];
 #endif
     constexpr bool ONES = (MODE == FWD_ONES_W);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -220,7 +221,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const int vi = blockIdx.y;
     if (vi >= V.count) return;
     const int v = V.start + vi * V.stride;
-    const int sb0 = blockIdx.x * F3_CPB;          // first detector column of the block
+    const int sb0 = blockIdx.x * (NW * F3_CPW);          // first detector column of the block
     const int s0 = sb0 + wid * F3_CPW;             // first detector column of the warp
     const float* __restrict__ x = xa;
     if (ctl && !PFX) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
@@ -241,8 +242,8 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     // copies into shared memory now (cp.async) so that the epilogue does not wait on HBM
     constexpr bool YW = (MODE != FWD_PLAIN);
     if (YW) {
-        for (int q = threadIdx.x; q < G.nt * F3_CPB; q += F3_BS) {
-            const int t = q / F3_CPB, c = q % F3_CPB;
+        for (int q = threadIdx.x; q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
+            const int t = q / (NW * F3_CPW), c = q % (NW * F3_CPW);
             const int ss = sb0 + c;
             if (ss >= G.ns) continue;
             const size_t a = ((size_t)v * G.nt + t) * G.ns + ss;
@@ -449,8 +450,8 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     if (YW) asm volatile("cp.async.wait_all;" ::: "memory");
 #endif
     __syncthreads();
-    for (int q = threadIdx.x; q < G.nt * F3_CPB; q += F3_BS) {
-        const int t = q / F3_CPB, c = q % F3_CPB;
+    for (int q = threadIdx.x; q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
+        const int t = q / (NW * F3_CPW), c = q % (NW * F3_CPW);
         const int ss = sb0 + c;
         if (ss >= G.ns) continue;
         const float lz = ray_Lz<ARC>(G, ss, t);
@@ -474,28 +475,39 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 }
 
+template <bool ARC, int MODE, bool PFX, int NW>
+static void fwd3_nw(const DGeom& G, int max_count, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
+                    const float* xb, const float* y, const float* w, float* out, int ps, cudaStream_t s) {
+    dim3 grid((G.ns + NW * F3_CPW - 1) / (NW * F3_CPW), max_count);
+    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    else k_fwd3<ARC, MODE, 4, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+}
+
+// 2-warp blocks when 4-warp blocks would fill fewer than two waves (8 blocks per SM)
 template <bool ARC, int MODE, bool PFX>
-static void fwd3_rpl(const DGeom& G, dim3 grid, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
+static void fwd3_rpl(const DGeom& G, int max_count, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
                      const float* xb, const float* y, const float* w, float* out, int ps, cudaStream_t s) {
-    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
-    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
-    else k_fwd3<ARC, MODE, 4, PFX><<<grid, F3_BS, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    const long long blocks4 = (long long)((G.ns + F3_CPB - 1) / F3_CPB) * max_count;
+    if (blocks4 < 148LL * F3_MINB * 2)
+        fwd3_nw<ARC, MODE, PFX, F3_NWARPS / 2>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, ps, s);
+    else
+        fwd3_nw<ARC, MODE, PFX, F3_NWARPS>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, ps, s);
 }
 
 template <bool ARC>
 static void fwd3_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                           const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
                           int pfx_stride, cudaStream_t s) {
-    dim3 grid((G.ns + F3_CPB - 1) / F3_CPB, max_count);
     const bool pfx = pfx_stride > 0;
     if (mode == FWD_PLAIN) {
-        pfx ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
-            : fwd3_rpl<ARC, FWD_PLAIN, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
+        pfx ? fwd3_rpl<ARC, FWD_PLAIN, true>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
+            : fwd3_rpl<ARC, FWD_PLAIN, false>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     } else if (mode == FWD_RESID) {
-        pfx ? fwd3_rpl<ARC, FWD_RESID, true>(G, grid, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
-            : fwd3_rpl<ARC, FWD_RESID, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
+        pfx ? fwd3_rpl<ARC, FWD_RESID, true>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, pfx_stride, s)
+            : fwd3_rpl<ARC, FWD_RESID, false>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     } else {
-        fwd3_rpl<ARC, FWD_ONES_W, false>(G, grid, vtab, ctl, v, xa, xb, y, w, out, 0, s);
+        fwd3_rpl<ARC, FWD_ONES_W, false>(G, max_count, vtab, ctl, v, xa, xb, y, w, out, 0, s);
     }
 }
 
