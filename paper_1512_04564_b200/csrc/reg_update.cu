@@ -126,7 +126,9 @@ enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
 __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__ pfx, const float* xs, float* tot,
                                              float run, int c, int lane, bool act, unsigned col, int k0, int k1) {
     tot[c * 32 + lane] = run;
-    __syncthreads();
+    // only the NZC chunk-warps of this row exchange totals (xs is per thread): a named
+    // barrier per row instead of the whole block
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.z), "r"(32 * (int)blockDim.y) : "memory");
     float P = 0.f;
     for (int q = 0; q < c; q++) P += tot[q * 32 + lane];
     if (!act) return;
