@@ -50,8 +50,20 @@ def peaks():
         p.update(hbm_gbs=m["hbm_gbs"], sm_max_mhz=m.get("sm_max_mhz", 1965.0), source="MEASURED_PEAKS.json")
     except Exception:
         pass
-    # FP32 (non-tensor) peak from unit counts and the max SM clock
+    # FP32 (non-tensor) peak: the FFMA microbenchmark measured on this pool's B200 (scripts/fp32_peak.cu,
+    # profiles/fp32_peak.json; sustained = back-to-back launches for ~4 s, the figure for a kernel timed
+    # inside a long step), else the unit-count figure 148 SM x 128 lanes x 2 x max SM clock
     p["fp32_tflops"] = N_SM * FP32_LANES_PER_SM * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    p["fp32_source"] = "148 SM x 128 FP32 lanes x 2 x %.0f MHz (unit count, not measured)" % p["sm_max_mhz"]
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp32_peak.json")) as f:
+            m = json.load(f)
+        p["fp32_tflops"] = m["fp32_tflops_sustained"]
+        p["fp32_burst_tflops"] = m["fp32_tflops"]
+        p["fp32_source"] = ("measured: profiles/fp32_peak.json (scripts/fp32_peak.cu FFMA loop, sustained %.1f, "
+                            "burst %.1f TFLOP/s)" % (m["fp32_tflops_sustained"], m["fp32_tflops"]))
+    except Exception:
+        pass
     return p
 
 
@@ -121,71 +133,115 @@ def make_inputs(cfg, device):
     return dict(y=data["y"].to(f32), w=data["w"].to(f32), x0=data["x0"].to(f32), reg=reg)
 
 
-# ----------------------------------------------------------------------------- reference arm
-def oracle_step_sample(cfg, inputs_np, frac, rng_seed=0):
-    """One bounded sample of a sub-iteration with the float64 oracle (as it stands):
-    Algorithm 1 line 4-8 restricted to a fraction `frac` of subset 0's views and
-    the same fraction of z-slices for the regulariser/update.  Returns seconds."""
+# ----------------------------------------------------------------------------- the oracle, timed
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _oracle_state(cfg, inputs, k=5):
+    """Oracle problem + a seeded state (x0, g, h, D_L stand-in) for timing sub-iteration k+1.
+    D_L = A'WA1 costs as much as a whole outer iteration of projections; a positive constant
+    stands in for it (the work of a sub-iteration does not depend on its values)."""
+    import numpy as np
+
+    from oracle import alg
+    y = inputs["y"].double().cpu().numpy()
+    w = inputs["w"].double().cpu().numpy()
+    x0 = inputs["x0"].double().cpu().numpy()
+    reg = inputs["reg"]
+    prob = alg.Problem(cfg["geom"], y, w, reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"])
+    rng = np.random.default_rng(0)
+    gg = rng.standard_normal(x0.shape) * 1e-3
+    h = rng.standard_normal(x0.shape) * 1e-3
+    DL = np.full(x0.shape, 1e6)
+    return prob, x0, gg, h, DL
+
+
+def oracle_full_subiter(cfg, inputs, k=5):
+    """One whole sub-iteration (Algorithm 1 lines 4-9) of the float64
+    oracle as it stands (oracle.alg.alg1_run), subset m = k mod M.  Returns seconds."""
+    from oracle import alg
+    prob, x0, gg, h, DL = _oracle_state(cfg, inputs, k)
+    t0 = time.perf_counter()
+    alg.alg1_run(prob, x0, gg, h, k, 1, cfg["solver"]["M"], cfg["solver"]["alpha"], DL)
+    return time.perf_counter() - t0
+
+
+def oracle_sample(cfg, inputs, frac, k=5, state=None):
+    """A bounded sample of sub-iteration k+1 with the oracle's own functions: the
+    projector pair (line 6) on every q-th view of subset m = k mod M (views spread over the
+    whole subset, so the helix ends are represented), the regulariser and updates (lines
+    4-5, 7-8) on a centred slab of the same fraction of z-slices.  Returns (seconds of a whole
+    sub-iteration extrapolated from each part by its own fraction, description)."""
     import numpy as np
 
     from oracle import alg
     from oracle import projector as P
+    prob, x0, gg, h, DL = state if state is not None else _oracle_state(cfg, inputs, k)
     g = cfg["geom"]
-    M = cfg["solver"]["M"]
-    na = g["na"]
-    vm = (na + M - 1) // M
-    nv = max(1, int(round(frac * vm)))
-    views = (0, M, nv)
-    y, w, x0, reg = inputs_np
-    shape = P.vol_shape(g)
-    nz = shape[0]
-    nzs = max(1, int(round(frac * nz))) if g["dim"] == 3 else 1
-    gs = dict(g, nz=nzs) if g["dim"] == 3 else g
-    xs = np.ascontiguousarray(x0[:nzs])
-    rng = np.random.default_rng(rng_seed)
-    gg = rng.standard_normal(xs.shape) * 1e-3
-    h = rng.standard_normal(xs.shape) * 1e-3
-    DL = np.full(xs.shape, 1e6)          # timing sample only: values do not change the work
+    M, alpha = cfg["solver"]["M"], cfg["solver"]["alpha"]
+    m = k % M
+    vm = (g["na"] - m + M - 1) // M
+    nv = max(1, min(vm, int(round(frac * vm))))
+    q = max(1, vm // nv)
+    views = (m, M * q, nv)
+    nz = x0.shape[0]
+    nzs = max(1, min(nz, int(round(frac * nz)))) if g["dim"] == 3 else 1
+    z0 = (nz - nzs) // 2
+    gs = dict(g, nz=nzs, offset_z=g["offset_z"] + (z0 + 0.5 * nzs - 0.5 * nz) * g["dz"]) if g["dim"] == 3 else g
+    sl = slice(z0, z0 + nzs)
+    xs, gss, hs, Ds = (np.ascontiguousarray(a[sl]) for a in (x0, gg, h, DL))
+    rho = alg.rho_k(k, alpha)
     t0 = time.perf_counter()
-    # lines 4-5 on the slab
-    _, gradR, DR = P.reg(gs, reg["potential"], reg["delta"], reg["betas"], reg["n_dirs"], xs)
-    rho, alpha = alg.rho_k(5, cfg["solver"]["alpha"]), cfg["solver"]["alpha"]
-    s = rho * (DL * xs - h) + (1 - rho) * gg
-    xn = np.maximum(xs - (s + gradR) / (rho * DL + DR), 0.0)
-    # line 6 on the sampled views (full volume: the projector needs it)
+    _, gradR, DR = P.reg(gs, prob.potential, prob.delta, prob.betas, prob.n_dirs, xs)
+    s = rho * (Ds * xs - hs) + (1 - rho) * gss
+    xn = alg._x_update(xs, s, gradR, rho * Ds + DR)
+    t_vol = time.perf_counter() - t0
+    t0 = time.perf_counter()
     Ax = P.forward(g, x0, views)
-    r = w[0:M * nv:M] * (Ax - y[0:M * nv:M])
+    rows = slice(m, m + M * q * nv, M * q)
+    r = prob.w[rows] * (Ax - prob.y[rows])
     zeta = M * P.back(g, r, views)
-    # lines 7-8 on the slab
-    zs = zeta[:nzs]
-    gg = rho / (rho + 1) * (alpha * zs + (1 - alpha) * gg) + gg / (rho + 1)
-    h = alpha * (DL * xn - zs) + (1 - alpha) * h
-    return time.perf_counter() - t0, nv, vm, nzs, nz
+    t_proj = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    zs = zeta[sl]
+    gss = rho / (rho + 1) * (alpha * zs + (1 - alpha) * gss) + gss / (rho + 1)
+    hs = alpha * (Ds * xn - zs) + (1 - alpha) * hs
+    t_vol += time.perf_counter() - t0
+    est = t_proj * vm / nv + t_vol * nz / nzs
+    desc = ("Alg. 1 lines 4-9 of subset %d: projector pair on %d of its %d views (every %d-th), regulariser and "
+            "updates on %d of %d z-slices; each part extrapolated by its fraction" % (m, nv, vm, q, nzs, nz))
+    return est, desc
 
 
-def cpu_baseline(cfg, inputs, target_s=20.0, steps=1, warmup=0):
-    """Oracle timed on the host cores on a bounded sample; value in subset-iters/s."""
-    import numpy as np
-    y = inputs["y"].double().cpu().numpy()
-    w = inputs["w"].double().cpu().numpy()
-    x0 = inputs["x0"].double().cpu().numpy()
-    args = (y, w, x0, inputs["reg"])
-    # calibrate the sample fraction on a tiny probe
-    probe = 1.0 / max(1, (cfg["geom"]["na"] // cfg["solver"]["M"]))
-    tp, nv, vm, _, _ = oracle_step_sample(cfg, args, probe)
-    per_full = tp / (nv / vm)
-    frac = min(1.0, target_s / max(per_full, 1e-9))
-    for _ in range(warmup):
-        oracle_step_sample(cfg, args, frac)
-    tot, fr = 0.0, 0.0
-    for _ in range(steps):
-        t, nv, vm, nzs, nz = oracle_step_sample(cfg, args, frac)
-        tot += t
-        fr += nv / vm
-    val = fr / tot      # sub-iterations per second (linear extrapolation of the sample)
-    sample = ("per step: Alg. 1 lines 4-8 on %d of the %d views of subset 0 and %d of %d z-slices "
-              "(fraction %.4f of one sub-iteration)" % (nv, vm, nzs, nz, nv / vm))
-    return val, sample
+def cpu_baseline(cfg, inputs, single_thread_s=10.0):
+    """The oracle on the host cores: one whole timed sub-iteration on all cores (value), plus a
+    bounded single-thread sample extrapolated to one sub-iteration; subset-iters/s."""
+    from oracle import projector as P
+    P.build()
+    cores = P.max_threads()
+    t_all = oracle_full_subiter(cfg, inputs)
+    out = {"value": 1.0 / t_all, "unit": "subset-iters/s", "cores": cores, "kind": "oracle",
+           "sample": "one whole sub-iteration (Alg. 1 lines 4-9, oracle.alg.alg1_run, subset 5 of %d) on %d threads, "
+                     "%.2f s" % (cfg["solver"]["M"], cores, t_all),
+           "cpu_model": _cpu_model()}
+    try:
+        P.set_threads(1)
+        state = _oracle_state(cfg, inputs)
+        frac = min(1.0, single_thread_s / (t_all * cores))
+        est, desc = oracle_sample(cfg, inputs, frac, state=state)
+        out["value_1thread"] = 1.0 / est
+        out["sample_1thread"] = desc
+    finally:
+        P.set_threads(cores)
+    return out
 
 
 def run_reference(args):
@@ -201,9 +257,19 @@ def run_reference(args):
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     inputs = make_inputs(cfg, dev)
     M = cfg["solver"]["M"]
-    budget = 150.0
-    per_step = budget / max(1, args.steps + args.warmup)
-    val, sample = cpu_baseline(cfg, inputs, target_s=per_step, steps=args.steps, warmup=args.warmup)
+    # each step: a bounded sample of one sub-iteration (oracle_sample), sized so that the whole
+    # --steps/--warmup run takes ~150 s of oracle work; value = the mean of the extrapolated rates
+    state = _oracle_state(cfg, inputs)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    est, _ = oracle_sample(cfg, inputs, 0.02, state=state)   # probe (2% of a sub-iteration)
+    frac = min(1.0, budget / max(est, 1e-9))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, inputs, frac, state=state)
+    ests = []
+    for _ in range(args.steps):
+        e, sample = oracle_sample(cfg, inputs, frac, state=state)
+        ests.append(e)
+    val = len(ests) / sum(ests)
     cores = P.max_threads()
     line = {"impl": "reference", "metric": "relaxed OS-LALM subset-iters/s", "value": val,
             "unit": "subset-iters/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -211,7 +277,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config], "config": args.config},
             "cpu_baseline": {"value": val, "unit": "subset-iters/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": "per step: " + sample, "cpu_model": _cpu_model()},
             "e2e": {"value": val, "unit": "subset-iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -376,7 +442,7 @@ def run_cuda(args):
                 "algorithmic": "SURVEY 8d: 2 FLOP/nonzero + 6/in-cone voxel-view pair + 150/in-cone column-view "
                                "pair of A_m; per subset nnz %.4g, pairs %.4g, columns %.4g = %.4g FLOP"
                                % (nnz_sub, pvox_sub, pcol_sub, flop_sub),
-                "peak_source": "148 SM x 128 FP32 lanes x 2 x %.0f MHz (sm_max)" % pk["sm_max_mhz"]}
+                "peak_source": pk["fp32_source"]}
     else:
         byts = 24.0 * nvox
         achieved = byts / (per_launch_ms / 1e3) / 1e9
@@ -418,11 +484,7 @@ def run_cuda(args):
             kernels[key + "_issue_frac"] = wi / (kms[q] / M / 1e3) / (N_SM * 4 * pk["sm_max_mhz"] * 1e6)
     cb = None
     if world == 1 and not args.no_cpu_baseline:
-        from oracle import projector as P
-        P.build()
-        val, sample = cpu_baseline(cfg, inputs, target_s=args.cpu_seconds)
-        cb = {"value": val, "unit": "subset-iters/s", "cores": P.max_threads(), "kind": "oracle",
-              "sample": sample}
+        cb = cpu_baseline(cfg, inputs, single_thread_s=args.cpu_seconds)
     work_mb = (7 * nvox * 4 + 3 * rm * 4) / 2 ** 20
     line = {
         "metric": "relaxed OS-LALM subset-iters/s", "value": value, "unit": "subset-iters/s",
@@ -460,7 +522,8 @@ def main():
     ap.add_argument("--dist-path", action="store_true",
                     help="N=1 only: run the multi-GPU code path on a world-1 NCCL communicator")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="single-thread oracle sample length (the all-core figure is one whole sub-iteration)")
     args = ap.parse_args()
     if args.warmup < 1:
         raise SystemExit("--warmup must be >= 1")

@@ -168,6 +168,20 @@ void ct_geom_destroy(ct_geom* g);
  * x: volume; proj: float[v.count][nt][ns] (overwritten). */
 ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, float* proj, ct_stream s);
 
+/* p = A x on views v through the z-prefix path of the solver's forward
+ * projection (Algorithm 1 line 6): the cumulative sums
+ * of x along z are formed first (float2 (A_k, x_k) per voxel, z fastest,
+ * in the workspace) and each detector row's F2-weighted sum is one difference
+ * of the interpolated cumulative.  Same entries as ct_forward up to float32
+ * rounding; this is the kernel oslalm_relaxed_solve runs (with the residual
+ * epilogue instead of the plain one).  2-D geometries: same as ct_forward.
+ * workspace: device, 16-byte aligned, >= ct_zprefix_size bytes (contents
+ * overwritten).  Errors: CT_E_CONFIG (NULL, alignment), CT_E_SHAPE (views),
+ * CT_E_NOMEM (workspace), CT_E_CUDA. */
+ct_status ct_zprefix_size(const ct_geom* g, size_t* bytes);
+ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_views v, float* proj, void* workspace,
+                             size_t workspace_bytes, ct_stream s);
+
 /* x_out (=|+=) scale * A' proj on views v.
  * proj: float[v.count][nt][ns]; accumulate != 0 adds into x_out. */
 ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, int accumulate, float* x_out,
@@ -280,6 +294,17 @@ ct_status oslalm_profile(const ct_geom* g, const float* y, const float* w, const
                          const float* d_l, const oslalm_params* p, oslalm_state* st, int n_subiters,
                          const ct_dist* dist, void* workspace, size_t workspace_bytes, ct_stream s,
                          double* kernel_ms);
+
+/* The weighted residual of the most recent sub-iteration of a solve (Eq. 36 /
+ * Algorithm 1 line 6): r_out = W_m (A_m x+ - y_m) for the
+ * views of subset m = (k - 1) mod M held by this rank (rank p of G: the
+ * subset-local views p, p + G, ...), float[count][nt][ns].  k is the state's
+ * counter after the oslalm_relaxed_solve call that ran sub-iteration k, with
+ * the same g, p, dist and workspace (the residual lives in the workspace
+ * until the next call).  For inspection and parity tests.  Errors:
+ * CT_E_CONFIG (NULL, k < 1, params), CT_E_NOMEM (workspace), CT_E_CUDA. */
+ct_status oslalm_residual(const ct_geom* g, const oslalm_params* p, const ct_dist* dist, int64_t k,
+                          const void* workspace, size_t workspace_bytes, float* r_out, ct_stream s);
 
 /* *d_count (device uint64) += number of nonzero entries of A on views v:
  * entry ((v,t,s),(i,j,k)) != 0 iff F1(s) > 0 and F2(k,t) > 0.

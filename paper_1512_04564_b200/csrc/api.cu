@@ -111,6 +111,10 @@ static ct_status validate_desc(const ct_geom_desc* d) {
         !std::isfinite(d->source_z0))
         return fail(CT_E_CONFIG, "non-finite orbit parameters");
     if ((long long)d->nx * d->ny * d->nz >= (1LL << 32)) return fail(CT_E_CONFIG, "volume of 2^32 voxels or more");
+    // the 3-D forward addresses the z-prefix array (nx ny columns of round2(nz + 2) float2 entries)
+    // with 32-bit element offsets, and voxel columns j nx + i in int
+    if (d->dim == 3 && (long long)d->nx * d->ny * (((long long)d->nz + 2) & ~1LL) >= (1LL << 32))
+        return fail(CT_E_CONFIG, "z-prefix array of nx*ny*(nz+2) >= 2^32 entries");
     if (d->nt > 128) return fail(CT_E_CONFIG, "nt = %d > 128 detector rows", d->nt);
     // the update kernel keeps x+ of a 32-column tile in shared memory for the z-prefix
     if (d->nz > 1536) return fail(CT_E_CONFIG, "nz = %d > 1536 slices", d->nz);
@@ -243,6 +247,31 @@ extern "C" ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, fl
     DeviceGuard guard(g->device);
     launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, x, x, nullptr, nullptr, proj, FWD_PLAIN,
                (cudaStream_t)s);
+    return check_async();
+}
+
+extern "C" ct_status ct_zprefix_size(const ct_geom* g, size_t* bytes) {
+    if (!g || !bytes) return fail(CT_E_CONFIG, "ct_zprefix_size: NULL argument");
+    *bytes = g->G.dim == 3 ? sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G) : 0;
+    return CT_OK;
+}
+
+extern "C" ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_views v, float* proj, void* workspace,
+                                        size_t workspace_bytes, ct_stream s) {
+    if (!g || !x || !proj) return fail(CT_E_CONFIG, "ct_forward_zprefix: NULL argument");
+    ct_status st = check_views(g, v);
+    if (st != CT_OK) return st;
+    if (g->G.dim != 3) return ct_forward(g, x, v, proj, s);
+    size_t need = 0;
+    ct_zprefix_size(g, &need);
+    if (!workspace || workspace_bytes < need)
+        return fail(CT_E_NOMEM, "ct_forward_zprefix: workspace %zu < %zu bytes", workspace_bytes, need);
+    if ((uintptr_t)workspace % 16) return fail(CT_E_CONFIG, "ct_forward_zprefix: workspace not 16-byte aligned");
+    DeviceGuard guard(g->device);
+    float* pfx = (float*)workspace;
+    launch_zprefix(g->G, x, pfx, (cudaStream_t)s);
+    launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, pfx, pfx, nullptr, nullptr, proj, FWD_PLAIN,
+               (cudaStream_t)s, pfx_stride_of(g->G));
     return check_async();
 }
 
@@ -592,10 +621,15 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                 launch_advance(ctl, s);
             }
             if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
-            CT_CUDA(cudaEventRecord(dist->ev_x, s));
-            CT_CUDA(cudaStreamWaitEvent(dist->side, dist->ev_x, 0));
-            launch_reg(g->G, rp, xout, kappa, gradr, curvr, dist->side);
-            CT_CUDA(cudaEventRecord(dist->ev_sten, dist->side));
+            const bool last = done + 1 == n_subiters;
+            if (!last) {
+                // the stencil of x+ feeds the next sub-iteration of this call only: the last
+                // sub-iteration's fold (below) completes the state without it
+                CT_CUDA(cudaEventRecord(dist->ev_x, s));
+                CT_CUDA(cudaStreamWaitEvent(dist->side, dist->ev_x, 0));
+                launch_reg(g->G, rp, xout, kappa, gradr, curvr, dist->side);
+                CT_CUDA(cudaEventRecord(dist->ev_sten, dist->side));
+            }
             if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s,
                                pfx_stride_of(g->G));
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
@@ -604,7 +638,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
             CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
             pending = true;
-            if (done + 1 == n_subiters) {
+            if (last) {
                 // fold the last zeta (lines 7-8) and advance: the state is complete on return
                 launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
                 launch_advance(ctl, s);
@@ -666,6 +700,25 @@ extern "C" ct_status oslalm_profile(const ct_geom* g, const float* y, const floa
     if (!kernel_ms) return fail(CT_E_CONFIG, "oslalm_profile: kernel_ms is NULL");
     return solve_impl(g, y, w, r, kappa, d_l, p, st, n_subiters, nullptr, nullptr, dist, workspace,
                       workspace_bytes, stream, kernel_ms);
+}
+
+extern "C" ct_status oslalm_residual(const ct_geom* g, const oslalm_params* p, const ct_dist* dist, int64_t k,
+                                     const void* workspace, size_t workspace_bytes, float* r_out, ct_stream stream) {
+    if (!g || !workspace || !r_out) return fail(CT_E_CONFIG, "oslalm_residual: NULL argument");
+    ct_status st = validate_params(g, p);
+    if (st != CT_OK) return st;
+    if (k < 1) return fail(CT_E_CONFIG, "oslalm_residual: k = %lld, no sub-iteration done", (long long)k);
+    const WsLayout L = ws_layout(g, p, dist);
+    if (workspace_bytes < L.total) return fail(CT_E_NOMEM, "workspace %zu < %zu bytes", workspace_bytes, L.total);
+    const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
+    const int M = p->M, m = (int)((k - 1) % M);
+    const int vm = (g->d.na - m + M - 1) / M;
+    const int cnt = std::max(0, (vm - rank + world - 1) / world);
+    if (cnt == 0) return CT_OK;
+    DeviceGuard guard(g->device);
+    const float* rbuf = (const float*)((const char*)workspace + L.r);
+    launch_unfold_lz(g->G, cnt, rbuf, r_out, (cudaStream_t)stream);
+    return check_async();
 }
 
 extern "C" ct_status ct_count_nnz(const ct_geom* g, ct_views v, uint64_t* d_count, ct_stream s) {

@@ -28,6 +28,11 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
 // f in [k - 1/2, k + 1/2] is A_k + f x_k).  Column stride in float2 units: nz + 1 rounded up to even.
 __host__ __device__ inline int pfx_stride_of(const DGeom& G) { return ((G.nz + 1) + 1) & ~1; }
 
+// z-prefix array of x (same entries as the update kernel writes for x+), for ct_forward_zprefix
+void launch_zprefix(const DGeom& G, const float* x, float* pfx, cudaStream_t s);
+// r_out = r / L_z(s, t) over `count` views (the solver's residual buffer carries L_z for the back-projector)
+void launch_unfold_lz(const DGeom& G, int count, const float* r, float* r_out, cudaStream_t s);
+
 void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);
 

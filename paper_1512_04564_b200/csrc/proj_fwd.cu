@@ -10,6 +10,8 @@
 //   FWD_PLAIN  p = L_z q
 //   FWD_RESID  r = L_z w (L_z q - y)     -> back-projector needs no L_z
 //   FWD_ONES_W r = L_z w (L_z A0 1)      (D_L = A'WA1)
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace ctr {
@@ -520,6 +522,25 @@ static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Vi
     if (mode == FWD_PLAIN) k_fwd2<ARC, FWD_PLAIN><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
     else if (mode == FWD_RESID) k_fwd2<ARC, FWD_RESID><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
     else k_fwd2<ARC, FWD_ONES_W><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+}
+
+// r / L_z(s, t): the solver's residual buffer holds L_z W (A x - y) (L_z folded in for the
+// back-projector, which then needs none); oslalm_residual returns W (A x - y).
+template <bool ARC>
+__global__ void k_unfold_lz(DGeom G, long long n, const float* __restrict__ r, float* __restrict__ out) {
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n; q += (long long)gridDim.x * blockDim.x) {
+        const int s = (int)(q % G.ns);
+        const int t = (int)((q / G.ns) % G.nt);
+        out[q] = G.dim == 3 ? r[q] / ray_Lz<ARC>(G, s, t) : r[q];
+    }
+}
+
+void launch_unfold_lz(const DGeom& G, int count, const float* r, float* r_out, cudaStream_t s) {
+    const long long n = (long long)count * G.nt * G.ns;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    if (G.arc) k_unfold_lz<true><<<blocks, 256, 0, s>>>(G, n, r, r_out);
+    else k_unfold_lz<false><<<blocks, 256, 0, s>>>(G, n, r, r_out);
+    launches_add(1);
 }
 
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,

@@ -471,6 +471,26 @@ void launch_update_pre(const DGeom& G, const Ctl* ctl, const float* xin, float* 
     launches_add(1);
 }
 
+// z-prefix of an arbitrary image (ct_forward_zprefix): thread = voxel column, the same
+// (A_k, x_k) entries and rounding as write_prefix (one FFMA per entry, P summed in k order).
+__global__ void k_zprefix(DGeom G, const float* __restrict__ x, float* __restrict__ pfx) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= G.nxy) return;
+    float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + (size_t)col * (size_t)pfx_stride_of(G);
+    float P = 0.f;
+    for (int k = 0; k < G.nz; k++) {
+        const float xk = __ldg(x + (size_t)k * G.nxy + col);
+        pc[k] = make_float2(fmaf(0.5f - (float)k, xk, P), xk);
+        P += xk;
+    }
+    pc[G.nz] = make_float2(P, 0.f);
+}
+
+void launch_zprefix(const DGeom& G, const float* x, float* pfx, cudaStream_t s) {
+    k_zprefix<<<(unsigned)((G.nxy + 127) / 128), 128, 0, s>>>(G, x, pfx);
+    launches_add(1);
+}
+
 // ---- small elementwise kernels ----
 __global__ void k_gh_update(long long n, const Ctl* __restrict__ ctl, const float* __restrict__ zeta, float* g,
                             float* ht) {

@@ -70,7 +70,8 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "oslalm_workspace_size", "oslalm_relaxed_solve", "oslalm_state_h", "oslalm_rho", "ct_sync",
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
            "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
-           "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work"]
+           "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size", "ct_forward_zprefix",
+           "oslalm_residual"]
 
 _lib = None
 
@@ -89,6 +90,9 @@ def load():
     L.ct_geom_destroy.restype = None
     L.ct_forward.argtypes = [vp, vp, ct_views, vp, vp]
     L.ct_back.argtypes = [vp, vp, ct_views, f, ctypes.c_int, vp, vp]
+    L.ct_zprefix_size.argtypes = [vp, P(ctypes.c_size_t)]
+    L.ct_forward_zprefix.argtypes = [vp, vp, ct_views, vp, vp, ctypes.c_size_t, vp]
+    L.oslalm_residual.argtypes = [vp, P(oslalm_params), vp, ctypes.c_int64, vp, ctypes.c_size_t, vp, vp]
     L.ct_sqs_diag.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.ct_reg_grad.argtypes = [vp, P(ct_reg_desc), vp, vp, vp, vp, vp]
     L.ct_kappa_weights.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -120,7 +124,8 @@ def load():
                  "oslalm_workspace_size",
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
-                 "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work"):
+                 "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size",
+                 "ct_forward_zprefix", "oslalm_residual"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -193,6 +198,22 @@ def ct_geom_destroy(h):
 
 def ct_forward(geom, x, v, proj, stream=None):
     _check(load().ct_forward(geom, _ptr(x), v, _ptr(proj), _stream(stream)))
+
+
+def ct_zprefix_size(geom):
+    n = ctypes.c_size_t()
+    _check(load().ct_zprefix_size(geom, ctypes.byref(n)))
+    return n.value
+
+
+def ct_forward_zprefix(geom, x, v, proj, workspace, stream=None):
+    _check(load().ct_forward_zprefix(geom, _ptr(x), v, _ptr(proj), ctypes.c_void_p(workspace.data_ptr()),
+                                     workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def oslalm_residual(geom, p, k, workspace, r_out, dist=None, stream=None):
+    _check(load().oslalm_residual(geom, ctypes.byref(p), dist, int(k), ctypes.c_void_p(workspace.data_ptr()),
+                                  workspace.numel() * workspace.element_size(), _ptr(r_out), _stream(stream)))
 
 
 def ct_back(geom, proj, v, x_out, scale=1.0, accumulate=False, stream=None):

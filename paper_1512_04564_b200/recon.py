@@ -178,6 +178,9 @@ class HostPipeline:
         else:
             # sub-iteration by sub-iteration, each after its subset's copy (k = 0 also reads subset M-1)
             M = rec.params.M
+            if rec.dl is None or (rec.state.k == 0 and rec.params.init_grad == C.INIT_FULL):
+                # D_L (all views) or the full-gradient line 1 reads every subset: the whole copy first
+                self.comp.wait_event(self.copied[b])
             for _ in range(n_subiters):
                 k = rec.state.k
                 if k == 0:

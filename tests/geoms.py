@@ -39,3 +39,46 @@ def tiny(kind, **over):
 
 KINDS = ["fan2d_arc", "fan2d_flat", "axial_flat", "helical_arc"]
 FINE_KINDS = ["helical_fine", "axial_fine"]  # GPU parity only (wide-footprint code paths)
+
+
+def mid(kind, **over):
+    """Mid-size geometries that select the kernel instances the BASELINE 3-D configs
+    run (the tiny ones above only reach the smallest):
+      helical_mid   arc, nt = 64 (two rows per lane in the forward), 160 columns x 240
+                    views per subset at M = 2 (>= 148 x 8 x 2 four-warp blocks: the 4-warp
+                    forward in the solve), nz = 56 (three 24-voxel back-projector z-chunks,
+                    the last ragged; two update z-chunks with the per-row prefix exchange),
+                    H = 1.4-2.4 rows per voxel (24-voxel chunks span 34-58 rows: two
+                    40-row passes in the back-projector)
+      helical_rpl4  flat, nt = 96 (four rows per lane), 4-warp forward over all views
+      axial_mid     flat axial, nt = 40, nz = 50 (two update z-chunks)"""
+    if kind == "helical_mid":
+        g = _geom(dim=3, nx=36, ny=36, nz=56, dx=1.0, dy=1.0, dz=1.0, det="arc", ns=160, nt=64,
+                  ds=0.625, dt=1.0, offset_s=0.75, offset_t=-0.3, dso=100.0, dsd=180.0, na=480,
+                  orbit_deg=720.0, pitch=1.0)
+        g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 1.0, 720.0)
+    elif kind == "helical_rpl4":
+        g = _geom(dim=3, nx=32, ny=30, nz=60, dx=1.0, dy=1.0, dz=0.8, det="flat", ns=128, nt=96,
+                  ds=0.7, dt=0.8, offset_s=-0.6, offset_t=0.4, dso=100.0, dsd=180.0, na=300,
+                  orbit_deg=720.0, pitch=0.9, orbit_start_deg=5.0)
+        g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 0.9, 720.0)
+    elif kind == "axial_mid":
+        g = _geom(dim=3, nx=40, ny=40, nz=50, dx=1.0, dy=1.0, dz=1.0, det="flat", ns=120, nt=40,
+                  ds=0.95, dt=1.6, offset_s=0.25, offset_t=0.1, dso=110.0, dsd=200.0, na=240)
+    else:
+        raise KeyError(kind)
+    g.update(over)
+    return copy.deepcopy(g)
+
+
+MID_KINDS = ["helical_mid", "helical_rpl4", "axial_mid"]
+
+
+def fwd3_blocks(g, count):
+    """Grid of the 3-D forward (proj_fwd.cu fwd3_rpl): 4-warp blocks of 16 detector columns
+    x views when that fills >= 2 waves of 8 blocks per SM on 148 SMs, else 2-warp blocks;
+    rows per lane RPL = 1 / 2 / 4 for nt <= 32 / 64 / 128."""
+    b4 = -(-g["ns"] // 16) * count
+    nw = 4 if b4 >= 148 * 8 * 2 else 2
+    rpl = 1 if g["nt"] <= 32 else 2 if g["nt"] <= 64 else 4
+    return nw, rpl

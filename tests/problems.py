@@ -42,8 +42,18 @@ def synthetic_problem(geom, seed=0, I0=1e4, n_dirs=None, potential="hyperbola", 
                 solver=dict(M=M, alpha=alpha))
 
 
-def config_problem(name, device="cpu", **shrink):
-    """A BASELINE config's seeded inputs (synth) with oracle D_L and betas."""
+def input_fingerprint(pb):
+    """Fingerprints of a problem's inputs (y, w, x0): element count, sum and sum of
+    squares (float64) — a regenerated input set must reproduce them."""
+    out = {}
+    for k in ("y", "w", "x0"):
+        a = np.asarray(pb[k], dtype=np.float64)
+        out[k] = np.array([a.size, float(a.sum()), float((a * a).sum())])
+    return out
+
+
+def config_problem(name, device="cpu", with_DL=True, **shrink):
+    """A BASELINE config's seeded inputs (synth) with oracle D_L (with_DL) and betas."""
     from synth.configs import shrink as shrink_cfg
     cfg = get_config(name)
     if shrink:
@@ -53,7 +63,9 @@ def config_problem(name, device="cpu", **shrink):
     y = data["y"].cpu().numpy()
     w = data["w"].cpu().numpy()
     x0 = data["x0"].cpu().numpy()
-    DL = P.back(g, w * P.forward(g, np.ones(P.vol_shape(g))))
+    if not with_DL and cfg["reg"]["beta0"] is None:
+        raise ValueError("with_DL=False needs a calibrated beta0")
+    DL = P.back(g, w * P.forward(g, np.ones(P.vol_shape(g)))) if with_DL else None
     n_dirs = cfg["reg"]["n_dirs"]
     b0 = cfg["reg"]["beta0"] if cfg["reg"]["beta0"] is not None else beta0_from_DL(DL, g, n_dirs)
     betas = reg_betas(g, b0, n_dirs)

@@ -544,6 +544,34 @@ def test_full_size_subiteration_sampled(C, name):
     x32, g32, h32, dl32 = (np.asarray(np.float32(a), dtype=np.float64) for a in (x, gg, ht, dl))
     rec.run(1)
     xg, gg_gpu, ht_gpu = host(rec.x), host(rec.g), host(rec.htilde)
+    # the solver's weighted residual of this sub-iteration (the benched forward instance, graph
+    # launch) at 2048 sampled rays against the oracle's W (A x+ - y) of the GPU's own x+
+    m = k0 % M
+    vcount = (g["na"] - m + M - 1) // M
+    nt = g["nt"] if g["dim"] == 3 else 1
+    r = torch.empty((vcount, nt, g["ns"]), dtype=torch.float32, device="cuda")
+    C.oslalm_residual(rec.h, rec.params, rec.k, rec.ws, r)
+    rg = host(r)
+    nray = 2048
+    vi = rng.integers(0, vcount, nray)
+    ss = rng.integers(0, g["ns"], nray)
+    tt = rng.integers(0, nt, nray)
+    vv = m + M * vi
+    ax = P.forward_rays(g, xg, vv, ss, tt)
+    wv, yv = w[vv, tt, ss], y[vv, tt, ss]
+    err = np.linalg.norm(rg[vi, tt, ss] - wv * (ax - yv)) / np.linalg.norm(wv * ax)
+    assert err <= 1e-4, ("residual", err)
+    # both forward paths of the ABI on x0 at the same rays (all views of the subset)
+    views_c = C.views(m, M, vcount)
+    axo = P.forward_rays(g, x, vv, ss, tt)
+    pd = torch.empty_like(r)
+    C.ct_forward(rec.h, rec.x.copy_(torch.as_tensor(x, dtype=torch.float32)), views_c, pd)
+    assert rel(host(pd)[vi, tt, ss], axo) <= 1e-4, ("ct_forward", rel(host(pd)[vi, tt, ss], axo))
+    if g["dim"] == 3:
+        wsz = torch.empty(C.ct_zprefix_size(rec.h), dtype=torch.uint8, device="cuda")
+        C.ct_forward_zprefix(rec.h, rec.x, views_c, pd, wsz)
+        assert rel(host(pd)[vi, tt, ss], axo) <= 1e-4, ("zprefix", rel(host(pd)[vi, tt, ss], axo))
+        del wsz
     rec.close()
     # oracle, Alg. 1 lines 4-8 in the paper's variables (h = D_L x - htilde)
     prob = alg.Problem(g, y, w, reg["potential"], reg["delta"], reg["betas"], nd)
