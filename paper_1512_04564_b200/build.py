@@ -33,9 +33,11 @@ def up_to_date():
     return all(os.path.getmtime(d) <= t for d in deps())
 
 
-def build(force=False, verbose=False, extra=()):
-    """Each .cu compiles to an object in parallel (no cross-file device code), then one link."""
-    if not force and up_to_date():
+def build(force=False, verbose=False, extra=(), out=None):
+    """Each .cu compiles to an object in parallel (no cross-file device code), then one link.
+    out: another output path (tuning variants built with extra -D flags; not the product)."""
+    lib = out or LIB
+    if out is None and not force and up_to_date():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
     tmpdir = os.path.join(HERE, ".build%d" % os.getpid())
@@ -53,19 +55,19 @@ def build(force=False, verbose=False, extra=()):
     try:
         with ThreadPoolExecutor(max_workers=min(8, len(objs))) as ex:
             list(ex.map(compile_one, zip(sources(), objs)))
-        tmp = LIB + ".tmp%d" % os.getpid()
+        tmp = lib + ".tmp%d" % os.getpid()
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC"] + objs + \
               ["-o", tmp, "-lnccl", "-lcudart"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
     finally:
         for o in objs:
             if os.path.exists(o):
                 os.remove(o)
         os.rmdir(tmpdir)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
