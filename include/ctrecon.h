@@ -238,13 +238,18 @@ ct_status oslalm_workspace_size(const ct_geom* g, const oslalm_params* p, const 
  * (w NULL = ones).  d_l: D_L from ct_sqs_diag (required).  kappa NULL = ones.
  * x_ref / rms_per_iter (host double[], one entry per completed outer
  * iteration within this call) are optional; giving them synchronises.
- * dist != NULL shards each subset's views over the ranks and sums the partial
- * back-projections with ncclAllReduce (all ranks hold the full volume).
- * While the all-reduce of sub-iteration j is in flight, grad R and D_R of the
- * new x run on the communicator's side stream; sub-iteration j+1 then folds
- * zeta into g, htilde (lines 7-8) and updates x (lines 4-5) in one kernel.
- * The last zeta of a call is folded before the call returns, so a state
- * handed back is always complete (resumable on any rank count).
+ * dist != NULL shards each subset's views over the ranks (all ranks hold the
+ * full volume): the partial back-projections are reduce-scattered by
+ * z-slab (ncclReduceScatter, or grouped ncclReduce when nz % world != 0;
+ * 2-D images: ncclAllReduce), the owner of each slab folds zeta into g, htilde
+ * (lines 7-8) and updates x (lines 4-5) on its slab in one kernel, and x+ is
+ * all-gathered (ncclAllGather / grouped ncclBroadcast) before its z-prefix is
+ * rebuilt for the next forward.  grad R and D_R of the owner's slab of the new
+ * x run on the communicator's side stream while the projections and the
+ * reduction are in flight.  The last zeta of a call is folded and g, htilde
+ * are all-gathered before the call returns, so a state handed back is always
+ * complete and identical on every rank (resumable on any rank count).
+ * 3-D: world <= nz (CT_E_CONFIG otherwise).
  * Single-GPU calls replay a cached CUDA graph of one sub-iteration.
  * Errors: CT_E_CONFIG (alpha not in [1,2), rho_fixed <= 0, M < 1 or M > na,
  * box_lo > box_hi, bad regulariser), CT_E_NOMEM (workspace), CT_E_NUMERIC
@@ -347,6 +352,17 @@ ct_status ct_sync(ct_stream s);
  * (rank/world), CT_E_NCCL, CT_E_CUDA.  ct_dist_destroy frees all of it. */
 ct_status ct_nccl_unique_id(unsigned char id[128]);
 ct_status ct_dist_create(int rank, int world, const unsigned char id[128], int device, ct_dist** out);
+/* Single-process emulation of a `world`-rank view-sharded solve on one device
+ * (SURVEY.md §4 T4): passed as `dist`, the solver runs every rank's share of
+ * each subset (rank p: the subset-local views p, p + world, ...; the device
+ * picks them from its per-rank control block) into its own partial
+ * back-projection, sums the partials in rank order (the reduce-scatter), has
+ * each z-slab owner fold and update its slab (with halo planes from the
+ * neighbouring slabs), and rebuilds the z-prefix of the whole x+ (the
+ * all-gather is in place).  No NCCL.  ct_sqs_diag sums every rank's views the
+ * same way; oslalm_residual returns rank 0's residual.  Errors: CT_E_CONFIG
+ * (world outside [1, 64], device), CT_E_CUDA. */
+ct_status ct_dist_create_local(int world, int device, ct_dist** out);
 void ct_dist_destroy(ct_dist* d);
 
 /* Number of this library's kernel launches since load (for bench accounting). */

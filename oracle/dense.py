@@ -7,6 +7,9 @@
                         quadratic loss g(u) = 1/2||u - y||^2 (after the Eq. 36
                         substitution A <- W^{1/2}A, y <- W^{1/2}y).
 * `eq33`              — Eq. 33 on the same dense problem.
+* `literal_eq18`      — LALM with simple relaxation, Eq. 18
+                        with the relaxation variable of Eq. 10,
+                        the same quadratic loss: the M = 1 form of Algorithm 2.
 * `dense_pwls_quadratic` — the exact minimiser of Eq. 34 with a quadratic
                         potential, (A'WA + H_R)^{-1} A'W y, built from
                         finite-difference matrices C_i written out here.
@@ -67,6 +70,31 @@ def literal_eq25(A, y, DA, x0, alpha, rhos, psi_grad, psi_curv, lo=0.0):
         xs.append(x.copy())
         nus.append(nu.copy())
     return xs, nus
+
+
+def literal_eq18(A, y, DA, x0, alpha, rhos, psi_grad, psi_curv, lo=0.0):
+    """Eq. 18 iterates x_k for k = 0..len(rhos), written in (x, u, mu):
+      x+ = argmin phi(x) + Q_psi(x; x) - <mu, Ax> + rho/2 ||Ax - u||^2 + rho/2 ||x - x_k||_G^2,
+           G = D_A - A'A (Eq. 16): Hessian D_psi + rho D_A, so
+           x+ = [ (D_psi x_k - grad psi + A'mu + rho A'u + rho G x_k) / (D_psi + rho D_A) ]_Omega;
+      r  = alpha A x+ + (1 - alpha) u                                  (Eq. 10)
+      u+ = argmin 1/2||u - y||^2 + <mu, u> + rho/2 ||r - u||^2 = (y - mu + rho r) / (1 + rho);
+      mu+ = mu - rho (r - u+).
+    Initialisation u0 = A x0, mu0 = y - u0 (then A'(u - y) is Algorithm 2's g)."""
+    x = np.array(x0, dtype=np.float64)
+    u = A @ x
+    mu = y - u
+    xs = [x.copy()]
+    for rho in rhos:
+        gp = psi_grad(x)
+        Dp = psi_curv(x)
+        Gx = DA * x - A.T @ (A @ x)
+        x = np.maximum((Dp * x - gp + A.T @ mu + rho * (A.T @ u) + rho * Gx) / (Dp + rho * DA), lo)
+        r = alpha * (A @ x) + (1.0 - alpha) * u
+        u = (y - mu + rho * r) / (1.0 + rho)
+        mu = mu - rho * (r - u)
+        xs.append(x.copy())
+    return xs
 
 
 def eq33(A, y, DA, x0, alpha, rhos, psi_grad, psi_curv, lo=0.0):

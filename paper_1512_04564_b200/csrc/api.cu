@@ -69,11 +69,39 @@ struct ct_geom {
 };
 
 struct ct_dist {
-    ncclComm_t comm;
+    ncclComm_t comm;                // NULL for a local (single-process) emulation
     int rank, world, device;
-    cudaStream_t side;              // high-priority stream: stencil of the new x during the all-reduce
+    cudaStream_t side;              // high-priority stream: stencil of the new x during the reduction
     cudaEvent_t ev_x, ev_sten;      // x+ written / stencil done
+    bool local;                     // ct_dist_create_local: this process plays all `world` ranks
 };
+
+// Owner slab of rank q of W (the plane range of ct_zslab_range): 3-D volumes split their z-planes;
+// 2-D images are not split (every rank owns the whole image and the partial gradients are
+// all-reduced instead of reduce-scattered).
+static void owner_slab(const DGeom& G, int q, int W, int* z0, int* nz) {
+    if (G.dim != 3) {
+        *z0 = 0;
+        *nz = G.nz;
+        return;
+    }
+    const int a = (int)((long long)q * G.nz / W), b = (int)((long long)(q + 1) * G.nz / W);
+    *z0 = a;
+    *nz = b - a;
+}
+
+// local ranks whose work this process runs (all of them in a local emulation)
+static int local_ranks(const ct_dist* dist) { return dist && dist->local ? dist->world : 1; }
+
+static DGeom sub_geom(const DGeom& G, int z0, int nzs) {
+    DGeom S = G;
+    S.nz = nzs;
+    S.z0 = G.z0 + (float)z0 * G.dz;
+    S.zbot = G.zbot + (float)z0 * G.dz;
+    S.ztop = S.zbot + (float)nzs * G.dz;
+    S.nvox = S.nxy * nzs;
+    return S;
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -294,20 +322,24 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
     if (chunk < 1) return fail(CT_E_NOMEM, "ct_sqs_diag: workspace %zu < %zu bytes", workspace_bytes, per_view);
     DeviceGuard guard(g->device);
     cudaStream_t cs = (cudaStream_t)s;
-    const int rank = dist ? dist->rank : 0, world = dist ? dist->world : 1;
+    const int world = dist ? dist->world : 1;
     CT_CUDA(cudaMemsetAsync(d_out, 0, sizeof(float) * g->G.nvox, cs));
-    // this rank's views: rank, rank + world, ...
-    const int mine = (g->d.na - rank + world - 1) / world;
+    // this rank's views: rank, rank + world, ... (a local emulation runs every rank's share in turn)
+    const int q0 = dist && !dist->local ? dist->rank : 0, q1 = dist && !dist->local ? q0 + 1 : local_ranks(dist);
     float* r = (float*)workspace;
-    for (int c0 = 0; c0 < mine; c0 += chunk) {
-        const int cnt = std::min(chunk, mine - c0);
-        Views vv{rank + c0 * world, world, cnt};
-        launch_fwd(g->G, g->vtab, nullptr, vv, cnt, nullptr, nullptr, nullptr, w, r, FWD_ONES_W, cs);
-        launch_back(g->G, g->vtab, nullptr, vv, r, 1.0f, BK_ACCUM, false, d_out, nullptr, nullptr, cs);
+    for (int rank = q0; rank < q1; rank++) {
+        const int mine = (g->d.na - rank + world - 1) / world;
+        for (int c0 = 0; c0 < mine; c0 += chunk) {
+            const int cnt = std::min(chunk, mine - c0);
+            Views vv{rank + c0 * world, world, cnt};
+            launch_fwd(g->G, g->vtab, nullptr, vv, cnt, nullptr, nullptr, nullptr, w, r, FWD_ONES_W, cs);
+            launch_back(g->G, g->vtab, nullptr, vv, r, 1.0f, BK_ACCUM, false, d_out, nullptr, nullptr, cs);
+        }
     }
     ct_status st = check_async();
     if (st != CT_OK) return st;
-    if (dist) CT_NCCL(ncclAllReduce(d_out, d_out, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, cs));
+    if (dist && !dist->local)
+        CT_NCCL(ncclAllReduce(d_out, d_out, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, cs));
     return CT_OK;
 }
 
@@ -391,26 +423,29 @@ extern "C" ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const f
 
 // ------------------------------------------------------------------ solver
 struct WsLayout {
-    size_t ctl, xalt, xt, r, zeta, gradr, curvr, flag, dsum, total;
+    size_t ctl, xalt, xt, r, r_stride, zeta, zeta_stride, gradr, curvr, flag, dsum, total;
 };
 
 
 static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dist* dist) {
     const int world = dist ? dist->world : 1;
+    const int nl = local_ranks(dist);
     const long long vm = (g->d.na + p->M - 1) / p->M;
     const long long vrank = (vm + world - 1) / world;
     WsLayout L;
     size_t off = 0;
-    L.ctl = off;
-    off = align_up(off + sizeof(Ctl));
+    L.ctl = off;   // one control block per local rank (view selection differs by rank)
+    off = align_up(off + sizeof(Ctl) * nl);
     L.xalt = off;
     off = align_up(off + sizeof(float) * g->G.nvox);
     L.xt = off;  // z-prefix array of x+ for the 3-D forward projector
     if (g->G.dim == 3) off = align_up(off + sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G));
-    L.r = off;
-    off = align_up(off + sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
-    L.zeta = off;
-    if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
+    L.r = off;     // residual of each local rank's views
+    L.r_stride = align_up(sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
+    off += L.r_stride * nl;
+    L.zeta = off;  // partial back-projection of each local rank (summed in place into the first)
+    L.zeta_stride = align_up(sizeof(float) * g->G.nvox);
+    if (dist) off += L.zeta_stride * nl;
     L.gradr = off;  // multi-GPU: grad R and D_R of the new x, computed during the all-reduce
     if (dist) off = align_up(off + sizeof(float) * g->G.nvox);
     L.curvr = off;
@@ -491,6 +526,10 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     float* xt = g->G.dim == 3 ? (float*)(ws + L.xt) : nullptr;
     float* rbuf = (float*)(ws + L.r);
     float* zeta = dist ? (float*)(ws + L.zeta) : nullptr;
+    const int nl = local_ranks(dist);
+    const long long zstride = (long long)(L.zeta_stride / sizeof(float)), rstride = (long long)(L.r_stride / sizeof(float));
+    if (dist && g->G.dim == 3 && dist->world > g->G.nz)
+        return fail(CT_E_CONFIG, "%d ranks for %d planes (each rank owns a z-slab)", dist->world, g->G.nz);
     float* gradr = dist ? (float*)(ws + L.gradr) : nullptr;
     float* curvr = dist ? (float*)(ws + L.curvr) : nullptr;
     int* dflag = (int*)(ws + L.flag);
@@ -503,48 +542,57 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         return fail(CT_E_SHAPE, "subset projection block exceeds 2^31 elements (increase M)");
     const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
 
-    Ctl h;
-    memset(&h, 0, sizeof(h));
-    h.k = st->k;
-    h.k_base = st->k;
-    h.M = M;
-    h.na = g->d.na;
-    h.rank = rank;
-    h.world = world;
-    h.rho_fixed_mode = p->rho_mode == OSLALM_RHO_FIXED;
-    h.simple = p->variant == OSLALM_SIMPLE;
-    h.alpha = (float)p->alpha;
-    h.rho_fixed = (float)p->rho_fixed;
-    CT_CUDA(cudaMemcpyAsync(ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, s));
+    std::vector<Ctl> hctl(nl);
+    for (int q = 0; q < nl; q++) {
+        Ctl& h = hctl[q];
+        memset(&h, 0, sizeof(h));
+        h.k = st->k;
+        h.k_base = st->k;
+        h.M = M;
+        h.na = g->d.na;
+        h.rank = dist && dist->local ? q : rank;
+        h.world = world;
+        h.rho_fixed_mode = p->rho_mode == OSLALM_RHO_FIXED;
+        h.simple = p->variant == OSLALM_SIMPLE;
+        h.alpha = (float)p->alpha;
+        h.rho_fixed = (float)p->rho_fixed;
+    }
+    // pageable source: the copy is staged before cudaMemcpyAsync returns
+    CT_CUDA(cudaMemcpyAsync(ctl, hctl.data(), sizeof(Ctl) * nl, cudaMemcpyHostToDevice, s));
 
     // ---- line 1: rho = 1, zeta = g = M grad L_M(x), h = D_L x - zeta  (htilde = zeta)
     if (st->k == 0) {
         float* zdst = dist ? zeta : st->g;
-        if (p->init_grad == OSLALM_INIT_LAST_SUBSET) {
-            const int m = M - 1;
-            const int vm = (g->d.na - m + M - 1) / M;
-            const int cnt = (vm - rank + world - 1) / world;
-            Views vv{m + rank * M, world * M, cnt};
-            if (cnt > 0) {
-                launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
-                launch_back(g->G, g->vtab, nullptr, vv, rbuf, (float)M, BK_WRITE, false, zdst, nullptr, nullptr, s);
+        // every local rank's partial gradient is accumulated in rank order into zdst
+        bool first = true;
+        for (int q = 0; q < nl; q++) {
+            const int rk = dist && dist->local ? q : rank;
+            if (p->init_grad == OSLALM_INIT_LAST_SUBSET) {
+                const int m = M - 1;
+                const int vm = (g->d.na - m + M - 1) / M;
+                const int cnt = (vm - rk + world - 1) / world;
+                Views vv{m + rk * M, world * M, cnt};
+                if (cnt > 0) {
+                    launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
+                    launch_back(g->G, g->vtab, nullptr, vv, rbuf, (float)M, first ? BK_WRITE : BK_ACCUM, false, zdst,
+                                nullptr, nullptr, s);
+                    first = false;
+                }
             } else {
-                CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
+                const int mine = (g->d.na - rk + world - 1) / world;
+                for (int c0 = 0; c0 < mine; c0 += max_count) {
+                    const int cnt = std::min(max_count, mine - c0);
+                    Views vv{rk + c0 * world, world, cnt};
+                    launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
+                    launch_back(g->G, g->vtab, nullptr, vv, rbuf, 1.0f, first ? BK_WRITE : BK_ACCUM, false, zdst,
+                                nullptr, nullptr, s);
+                    first = false;
+                }
             }
-        } else {
-            const int mine = (g->d.na - rank + world - 1) / world;
-            bool first = true;
-            for (int c0 = 0; c0 < mine; c0 += max_count) {
-                const int cnt = std::min(max_count, mine - c0);
-                Views vv{rank + c0 * world, world, cnt};
-                launch_fwd(g->G, g->vtab, nullptr, vv, cnt, st->x, st->x, y, w, rbuf, FWD_RESID, s);
-                launch_back(g->G, g->vtab, nullptr, vv, rbuf, 1.0f, first ? BK_WRITE : BK_ACCUM, false, zdst,
-                            nullptr, nullptr, s);
-                first = false;
-            }
-            if (first) CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
         }
-        if (dist) CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+        if (first) CT_CUDA(cudaMemsetAsync(zdst, 0, sizeof(float) * g->G.nvox, s));
+        if (dist && !dist->local)
+            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
         launch_init_from_zeta(g->G, zdst, st->g, st->htilde, s);
         stt = check_async();
         if (stt != CT_OK) return stt;
@@ -588,6 +636,53 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         evs.resize((size_t)n_subiters * 5);
         for (auto& e : evs) CT_CUDA(cudaEventCreate(&e));
     }
+    // multi-GPU: the owner slabs this process updates (all of them in a local emulation) and the
+    // collectives of the partial-gradient reduction
+    // (2-D: one owner of the whole image on every rank: the update is replicated after the all-reduce)
+    const bool split = g->G.dim == 3;
+    const int own0 = split && dist && !dist->local ? rank : 0;
+    const int own1 = !split ? 1 : dist && !dist->local ? rank + 1 : nl;
+    auto reduce_partials = [&](cudaStream_t cs) -> ct_status {
+        const DGeom& G = g->G;
+        if (dist->local) {
+            if (nl > 1) launch_sum_partials(zeta, nl, zstride, G.nvox, cs);
+            return check_async();
+        }
+        if (G.dim != 3 || world == 1) {
+            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)G.nvox, ncclFloat, ncclSum, dist->comm, cs));
+        } else if (G.nz % world == 0) {
+            const size_t cnt = (size_t)(G.nz / world) * G.nxy;
+            CT_NCCL(ncclReduceScatter(zeta, zeta + (size_t)rank * cnt, cnt, ncclFloat, ncclSum, dist->comm, cs));
+        } else {
+            CT_NCCL(ncclGroupStart());
+            for (int q = 0; q < world; q++) {
+                int a, nzq;
+                owner_slab(G, q, world, &a, &nzq);
+                float* b = zeta + (size_t)a * G.nxy;
+                CT_NCCL(ncclReduce(b, b, (size_t)nzq * G.nxy, ncclFloat, ncclSum, q, dist->comm, cs));
+            }
+            CT_NCCL(ncclGroupEnd());
+        }
+        return CT_OK;
+    };
+    auto all_gather = [&](float* buf, cudaStream_t cs) -> ct_status {
+        const DGeom& G = g->G;
+        if (dist->local || G.dim != 3 || world == 1) return CT_OK;   // every slab already in place
+        if (G.nz % world == 0) {
+            const size_t cnt = (size_t)(G.nz / world) * G.nxy;
+            CT_NCCL(ncclAllGather(buf + (size_t)rank * cnt, buf, cnt, ncclFloat, dist->comm, cs));
+        } else {
+            CT_NCCL(ncclGroupStart());
+            for (int q = 0; q < world; q++) {
+                int a, nzq;
+                owner_slab(G, q, world, &a, &nzq);
+                float* b = buf + (size_t)a * G.nxy;
+                CT_NCCL(ncclBroadcast(b, b, (size_t)nzq * G.nxy, ncclFloat, q, dist->comm, cs));
+            }
+            CT_NCCL(ncclGroupEnd());
+        }
+        return CT_OK;
+    };
     bool pending = false;  // multi-GPU: zeta of the previous sub-iteration not yet folded into g, htilde
     while (done < n_subiters) {
         cudaEvent_t* ev = kernel_ms ? &evs[(size_t)done * 5] : nullptr;
@@ -607,41 +702,81 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             launch_advance(ctl, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
         } else {
-            // Multi-GPU sub-iteration.  The stencil of the new x runs on the
-            // side stream while this rank's projections and the zeta all-reduce proceed; the
-            // next sub-iteration folds zeta into g, htilde and updates x in one pass.
+            // Multi-GPU sub-iteration: this rank's views are projected, the partial
+            // back-projections are reduce-scattered by z-slab (3-D; all-reduced in 2-D), the owner of
+            // each slab folds zeta into g, htilde and updates x on its slab only (the stencil of that
+            // slab ran on the side stream while the projections and the reduction were in flight),
+            // x+ is all-gathered and its z-prefix rebuilt for the next forward.  A local emulation
+            // (ct_dist_create_local) runs every rank's projections in turn into its own partial
+            // buffer, sums them in rank order and updates every slab: the same data flow on one GPU.
+            const DGeom& G = g->G;
             float* xin = (done & 1) ? xalt : st->x;
             float* xout = (done & 1) ? st->x : xalt;
-            if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
-            if (!pending) {
-                launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
-            } else {
-                CT_CUDA(cudaStreamWaitEvent(s, dist->ev_sten, 0));
-                launch_update_pre(g->G, ctl, xin, xout, d_l, st->g, st->htilde, zeta, gradr, curvr, lo, hi, xt, s);
-                launch_advance(ctl, s);
-            }
-            if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
             const bool last = done + 1 == n_subiters;
+            if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
+            if (pending) CT_CUDA(cudaStreamWaitEvent(s, dist->ev_sten, 0));
+            for (int q = own0; q < own1; q++) {
+                int a, nzq;
+                owner_slab(G, q, world, &a, &nzq);
+                if (nzq == 0) continue;
+                const size_t off = (size_t)a * G.nxy;
+                const DGeom S = sub_geom(G, a, nzq);
+                const bool hl = a > 0, hh = a + nzq < G.nz;
+                if (!pending)
+                    launch_update_halo(S, rp, ctl, st->x + off, xalt + off, d_l + off, st->g + off, st->htilde + off,
+                                       lo, hi, nullptr, hl, hh, s, kappa ? kappa + off : nullptr);
+                else
+                    launch_update_pre(S, ctl, xin + off, xout + off, d_l + off, st->g + off, st->htilde + off,
+                                      zeta + off, gradr + off, curvr + off, lo, hi, nullptr, s);
+            }
+            if (pending) launch_advance(ctl, s, nl);
+            stt = all_gather(xout, s);
+            if (stt != CT_OK) return stt;
+            if (xt) launch_zprefix(G, xout, xt, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
             if (!last) {
                 // the stencil of x+ feeds the next sub-iteration of this call only: the last
                 // sub-iteration's fold (below) completes the state without it
                 CT_CUDA(cudaEventRecord(dist->ev_x, s));
                 CT_CUDA(cudaStreamWaitEvent(dist->side, dist->ev_x, 0));
-                launch_reg(g->G, rp, xout, kappa, gradr, curvr, dist->side);
+                for (int q = own0; q < own1; q++) {
+                    int a, nzq;
+                    owner_slab(G, q, world, &a, &nzq);
+                    if (nzq == 0) continue;
+                    const size_t off = (size_t)a * G.nxy;
+                    launch_reg(sub_geom(G, a, nzq), rp, xout + off, kappa ? kappa + off : nullptr, gradr + off,
+                               curvr + off, dist->side, a > 0, a + nzq < G.nz);
+                }
                 CT_CUDA(cudaEventRecord(dist->ev_sten, dist->side));
             }
-            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s,
-                               pfx_stride_of(g->G));
-            else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
+            for (int q = 0; q < nl; q++) {
+                float* rq = rbuf + q * rstride;
+                if (xt) launch_fwd(G, g->vtab, ctl + q, Views{0, 1, 0}, max_count, xt, xt, y, w, rq, FWD_RESID, s,
+                                   pfx_stride_of(G));
+                else launch_fwd(G, g->vtab, ctl + q, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rq, FWD_RESID, s);
+            }
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
-            launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_WRITE, false, zeta, nullptr, nullptr, s);
+            for (int q = 0; q < nl; q++)
+                launch_back(G, g->vtab, ctl + q, Views{0, 1, 0}, rbuf + q * rstride, Mf, BK_WRITE, false,
+                            zeta + q * zstride, nullptr, nullptr, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
-            CT_NCCL(ncclAllReduce(zeta, zeta, (size_t)g->G.nvox, ncclFloat, ncclSum, dist->comm, s));
+            stt = reduce_partials(s);
+            if (stt != CT_OK) return stt;
             pending = true;
             if (last) {
-                // fold the last zeta (lines 7-8) and advance: the state is complete on return
-                launch_gh_update(g->G, ctl, zeta, st->g, st->htilde, s);
-                launch_advance(ctl, s);
+                // fold the last zeta (lines 7-8) on the owned slabs, advance, and replicate g, htilde:
+                // the state is complete (and identical on every rank) on return
+                for (int q = own0; q < own1; q++) {
+                    int a, nzq;
+                    owner_slab(G, q, world, &a, &nzq);
+                    if (nzq == 0) continue;
+                    const size_t off = (size_t)a * G.nxy;
+                    launch_gh_update(sub_geom(G, a, nzq), ctl, zeta + off, st->g + off, st->htilde + off, s);
+                }
+                launch_advance(ctl, s, nl);
+                stt = all_gather(st->g, s);
+                if (stt == CT_OK) stt = all_gather(st->htilde, s);
+                if (stt != CT_OK) return stt;
                 pending = false;
             }
             if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
@@ -804,7 +939,7 @@ extern "C" ct_status ct_dist_create(int rank, int world, const unsigned char id[
     memcpy(u.internal, id, 128);
     ncclComm_t comm;
     CT_NCCL(ncclCommInitRank(&comm, world, u, rank));
-    ct_dist* d = new ct_dist{comm, rank, world, device, nullptr, nullptr, nullptr};
+    ct_dist* d = new ct_dist{comm, rank, world, device, nullptr, nullptr, nullptr, false};
     int lo = 0, hi = 0;
     cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&d->side, cudaStreamNonBlocking, hi);
@@ -818,13 +953,35 @@ extern "C" ct_status ct_dist_create(int rank, int world, const unsigned char id[
     return CT_OK;
 }
 
+extern "C" ct_status ct_dist_create_local(int world, int device, ct_dist** out) {
+    if (!out) return fail(CT_E_CONFIG, "ct_dist_create_local: NULL argument");
+    *out = nullptr;
+    if (world < 1 || world > 64) return fail(CT_E_CONFIG, "local world %d outside [1, 64]", world);
+    int ndev = 0;
+    CT_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(CT_E_CONFIG, "device %d not present", device);
+    DeviceGuard guard(device);
+    ct_dist* d = new ct_dist{nullptr, 0, world, device, nullptr, nullptr, nullptr, true};
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&d->side, cudaStreamNonBlocking, hi);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_x, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d->ev_sten, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        ct_dist_destroy(d);
+        return fail(CT_E_CUDA, "ct_dist_create_local: %s", cudaGetErrorString(e));
+    }
+    *out = d;
+    return CT_OK;
+}
+
 extern "C" void ct_dist_destroy(ct_dist* d) {
     if (!d) return;
     DeviceGuard guard(d->device);
     if (d->ev_sten) cudaEventDestroy(d->ev_sten);
     if (d->ev_x) cudaEventDestroy(d->ev_x);
     if (d->side) cudaStreamDestroy(d->side);
-    ncclCommDestroy(d->comm);
+    if (d->comm) ncclCommDestroy(d->comm);
     delete d;
 }
 

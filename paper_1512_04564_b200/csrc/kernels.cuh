@@ -37,8 +37,9 @@ void launch_back(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, co
                  int epi, bool apply_lz, float* out, float* g, float* ht, cudaStream_t s);
 
 // regulariser gradient / curvature only (ct_reg_grad)
+// (halo_lo / halo_hi: planes -1 / nz of x exist, G a z-slab of a larger volume)
 void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad, float* curv,
-                cudaStream_t s);
+                cudaStream_t s, bool halo_lo = false, bool halo_hi = false);
 
 // fused stencil + x-update of Algorithm 1 lines 4-5, writes htilde partial
 void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
@@ -49,7 +50,7 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
 // (x buffers xa, xb point at plane 0 of (nz + 2)-plane allocations)
 void launch_update_halo(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                         float* g, float* ht, float box_lo, float box_hi, float* pfx, bool halo_lo, bool halo_hi,
-                        cudaStream_t s);
+                        cudaStream_t s, const float* kappa = nullptr);
 
 // multi-GPU path: fold the all-reduced zeta of the previous sub-iteration into
 // g, htilde (lines 7-8) and run lines 4-5 from precomputed grad R / D_R
@@ -69,7 +70,9 @@ void launch_kappa_ratio(long long n, const float* a, const float* b, float* kapp
 // dist path: g, htilde update from an all-reduced zeta (lines 7-8)
 void launch_gh_update(const DGeom& G, const Ctl* ctl, const float* zeta, float* g, float* ht, cudaStream_t s);
 void launch_init_from_zeta(const DGeom& G, const float* zeta, float* g, float* ht, cudaStream_t s);
-void launch_advance(Ctl* ctl, cudaStream_t s);
+void launch_advance(Ctl* ctl, cudaStream_t s, int n = 1);   // k += 1 in n consecutive control blocks
+// base[i] = sum_p base[p stride + i], p = 0..n-1 in order (emulated reduction of partial gradients)
+void launch_sum_partials(float* base, int n, long long stride, long long count, cudaStream_t s);
 void launch_state_h(const DGeom& G, const float* dl, const float* x, const float* ht, float* h, cudaStream_t s);
 // flag[0] |= any non-finite in x; optional sum of squares of (x - xref) into dsum[0]
 void launch_check(const DGeom& G, const float* x, const float* xref, int* flag, double* dsum, cudaStream_t s);

@@ -25,7 +25,6 @@ namespace ctr {
 #endif
 constexpr int BK_Y = BK_YDIM;
 constexpr int BK_BS = 32 * BK_Y;
-constexpr int BK_KZ_DEFAULT = 24;  // voxels per thread in z (tuning knob CTR_BK_KZ = 8 | 16 | 24 | 32)
 constexpr int BK_RMAX3 = 28;      // rows buffered per pass in k_back3 at KZ = 16 (more rows => several passes)
 
 // 2-D back-projection: thread = one pixel and every VS-th view of the subset
@@ -263,26 +262,39 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 }
             }
             cs[n * BK_BS] = make_float2(run, 0.f);
-            // R(u) at voxel boundary u = B0 + k H: v = u - (tw + 1/2) in [-1/2, n - 1/2],
+            // R(u) at voxel boundary u = B0 + k H: v = u - (tw + 1/2) clamped to [-1/2, n - 1/2],
             // o = round(v) (magic number), R = cs[o].x + v cs[o].y (affine form above;
-            // cs[n] = (C_n, 0))
-            // boundary q of the chunk sits at row unit B0 + (k0 + q) H; q is a compile-time
-            // constant after unrolling, so the position is one FFMA with an immediate
+            // cs[n] = (C_n, 0)).  The clamp is a saturation: v = n g - 1/2 with
+            // g = sat((q H + base + 1/2)/n) (FFMA.SAT; q is a compile-time constant after
+            // unrolling); v and o of two boundaries at a time in packed FP32 (FFMA2, FADD2), and
+            // the two voxels' increments R(q+1) - R(q) added with one FADD2.
             const float base = fmaf((float)k0, H, Bs - (float)tw);
-            const float vmax = (float)n - 0.5f;
-            auto R = [&](int q) {
-                const float vv = fminf(fmaxf(fmaf((float)q, H, base), -0.5f), vmax);
-                const float rm = __fadd_rn(vv, 12582912.0f);
-                const int o = __float_as_int(rm) - 0x4B400000;
-                const float2 c = cs[o * BK_BS];
-                return fmaf(vv, c.y, c.x);
+            const float fn = (float)n, rn = __fdividef(1.f, fn);
+            const float Hn = H * rn, bn = (base + 0.5f) * rn;
+            auto R2 = [&](int q) {   // boundaries q, q + 1
+                const float2 gg = make_float2(__saturatef(fmaf((float)q, Hn, bn)),
+                                              __saturatef(fmaf((float)(q + 1), Hn, bn)));
+                const float2 vv = fma2(gg, bcast2(fn), bcast2(-0.5f));
+                const float2 rm = add2(vv, bcast2(12582912.0f));
+                const float2 ca = cs[(__float_as_int(rm.x) - 0x4B400000) * BK_BS];
+                const float2 cb = cs[(__float_as_int(rm.y) - 0x4B400000) * BK_BS];
+                return make_float2(fmaf(vv.x, ca.y, ca.x), fmaf(vv.y, cb.y, cb.x));
             };
-            float Rlo = R(0);
+            float Rlo;
+            {
+                const float g0 = __saturatef(bn);
+                const float v0 = fmaf(g0, fn, -0.5f);
+                const float2 c0 = cs[(__float_as_int(__fadd_rn(v0, 12582912.0f)) - 0x4B400000) * BK_BS];
+                Rlo = fmaf(v0, c0.y, c0.x);
+            }
+            static_assert(BK_KZ % 2 == 0, "voxel pairs");
 #pragma unroll
-            for (int q = 0; q < BK_KZ; q++) {
-                const float Rhi = R(q + 1);
-                acc[q] += Rhi - Rlo;
-                Rlo = Rhi;
+            for (int q = 0; q < BK_KZ; q += 2) {
+                const float2 Rh = R2(q + 1);
+                const float2 a2 = add2(make_float2(acc[q], acc[q + 1]), make_float2(Rh.x - Rlo, Rh.y - Rh.x));
+                acc[q] = a2.x;
+                acc[q + 1] = a2.y;
+                Rlo = Rh.y;
             }
         }
     }
@@ -396,14 +408,10 @@ static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, V
     }
 }
 
-static int back_kz() {
-    static int kz = [] {
-        const char* e = getenv("CTR_BK_KZ");
-        const int v = e ? atoi(e) : BK_KZ_DEFAULT;
-        return (v == 8 || v == 16 || v == 24 || v == 32) ? v : BK_KZ_DEFAULT;
-    }();
-    return kz;
-}
+#ifndef BK_KZSEL
+#define BK_KZSEL 24    // voxels per thread in z (tuning variants: -DBK_KZSEL=8 | 16 | 32)
+#endif
+static int back_kz() { return BK_KZSEL; }
 
 template <bool ARC, int DIM>
 static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,

@@ -197,6 +197,20 @@ constexpr int F3_WARPS = F3_NWARPS;
 constexpr int F3_CPW = 4;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
+// Tuning experiment kept as a compile-time switch: consuming queued hits two at a
+// time in packed FP32 (FFMA2 / FADD2 across the pair) cuts the hit loop from ~33 to ~23.5
+// instructions per hit but ran slower (c4 fwd 2.72 ms unrolled 1, 3.00 ms unrolled 2, vs 2.51 ms
+// one hit at a time, r2d): the loop is bound by its prefix gathers, not by issue.
+#ifndef F3_PAIRS
+#define F3_PAIRS 0     // PFX: queued hits consumed two at a time in packed FP32
+#endif
+#ifndef F3_PUNROLL
+#define F3_PUNROLL 2   // pair-loop unroll
+#endif
+#ifndef F3_SUNROLL
+#define F3_SUNROLL 4   // single-hit loop unroll
+#endif
+constexpr int kF3PairUnroll = F3_PUNROLL, kF3SingleUnroll = F3_SUNROLL;
 #ifndef F3_PREYW
 #define F3_PREYW 1     // epilogue y, w copied into shared memory by cp.async at kernel start
 #endif
@@ -211,7 +225,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
     __shared__ float4 qL[NW][32];    // L for the 4 detector columns
-    __shared__ float4 qG[NW][32];    // PFX: (-B0/H, 1/H, col, -) ; direct: (B0, H, col, -)
+    __shared__ float4 qG[NW][32];    // PFX: (1/(H nz), -B0/(H nz), column offset, X(top)); direct: (B0, H, col, -)
     __shared__ float stage[32 * RPL][(NW * F3_CPW) + 1];
 #if F3_PREYW
     __shared__ float ysm[MODE == FWD_RESID ? 32 * RPL : 1][(NW * F3_CPW)];   // epilogue operands (cp.async)
@@ -297,7 +311,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         const float kr = xstep ? dry / drx : drx / dry;
         const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
         const float inv_do = 1.f / dob;
-        const float fnz = (float)G.nz;
+        const float fnz = (float)G.nz, rnz = 1.f / (float)G.nz;
 
         for (int sl0 = 0; sl0 < na_; sl0 += 32 / F3_SUB) {
             const int sl = sl0 + lane / F3_SUB, sub = lane % F3_SUB;
@@ -337,17 +351,21 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     }
                     // PFX: the top-boundary gather (lane 31's upper row edge) is issued before the
                     // transaxial footprint so that its latency overlaps that arithmetic
-                    float invH = 0.f, b0 = 0.f, ft = 0.f;
+                    float ih = 0.f, bg = 0.f, ft = 0.f;
+                    unsigned cbq = 0u;
                     float2 qt = make_float2(0.f, 0.f);
                     if (PFX && cand) {
-                        invH = __fdividef(1.f, f.H);
-                        // f' = (u - B0)/H - 1/2 (voxel coordinate minus 1/2); X at the top
-                        // boundary RPL*32 of the lanes' rows (lane 31 needs it)
-                        b0 = fmaf(-f.B0, invH, -0.5f);
-                        const float2* __restrict__ Qc = Q + (unsigned)(j * G.nx + i) * (unsigned)pfx_stride;
-                        ft = fminf(fmaxf(fmaf((float)(RPL * 32), invH, b0), -0.5f), fnz - 0.5f);
+                        // voxel coordinate minus 1/2 at row unit u: f = (u - B0)/H - 1/2, clamped to
+                        // [-1/2, nz - 1/2] as f = nz g - 1/2, g = sat(u ih + bg) in [0, 1]
+                        // (ih = 1/(H nz), bg = (1/2 - B0/H)/nz): one FFMA.SAT instead of two clamps
+                        const float invH = __fdividef(1.f, f.H);
+                        ih = invH * rnz;
+                        bg = fmaf(-f.B0, invH, 0.f) * rnz;
+                        cbq = (unsigned)(j * G.nx + i) * (unsigned)pfx_stride - 0x4B400000u;
+                        const float gt = __saturatef(fmaf((float)(RPL * 32), ih, bg));
+                        ft = fmaf(gt, fnz, -0.5f);
                         const float rt = __fadd_rn(ft, 12582912.0f);
-                        qt = __ldg(Qc + (__float_as_int(rt) - 0x4B400000));
+                        qt = __ldg(Q + (cbq + __float_as_uint(rt)));
                     }
                     if (cand) {
                         fp_trans<ARC>(G, cb, sb, fb, f);
@@ -365,7 +383,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                             const float Ls = PFX ? f.lxy * f.H : f.lxy;
                             eL = make_float4(Ls * Fc[0], Ls * Fc[1], Ls * Fc[2], Ls * Fc[3]);
                             if (PFX) {
-                                eG = make_float4(b0, invH, __int_as_float(j * G.nx + i), fmaf(ft, qt.y, qt.x));
+                                eG = make_float4(ih, bg, __uint_as_float(cbq), fmaf(ft, qt.y, qt.x));
                             } else {
                                 eG = make_float4(f.B0, f.H, __int_as_float(j * G.nx + i), 0.f);
                             }
@@ -373,33 +391,88 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     }
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, nz);
+                const int n = __popc(m);
                 if (nz) {
                     const int slot = __popc(m & lanemask_lt);
                     qL[wid][slot] = eL;
                     qG[wid][slot] = eG;
                 }
                 __syncwarp();
-                const int n = __popc(m);
-                for (int e = 0; e < n; e++) {
+                if (PFX && F3_PAIRS) {
+                    // Two queued voxel columns A, B at a time, packed FP32 (FFMA2 / FADD2) across them:
+                    // X(u) = A_k + f x_k (A_k = P_k - (k - 1/2) x_k, f the clamped voxel coordinate
+                    // minus 1/2, k = round(f) by the 1.5 2^23 magic number; either rounding of a tie
+                    // gives the same X: X is continuous and Q_nz = (P_nz, 0)) at the lane's RPL lower
+                    // row boundaries; the upper boundary of its last row is the next lane's first
+                    // (shuffle), lane 31 takes the producer's X(RPL 32).  Row sums Rs = X(t+1) - X(t)
+                    // times H (folded into L) are credited to the four detector columns two rows at a
+                    // time (FFMA2 with the column weight broadcast).  Unsigned 32-bit element offsets.
+#pragma unroll (kF3PairUnroll)
+                    for (int e = 0; e < n; e += 2) {
+                        // an odd count: the last pair repeats the last hit with zero weight (its
+                        // gathers hit the lines the first half just fetched)
+                        const int e1 = min(e + 1, n - 1);
+                        const float4 LA = qL[wid][e];
+                        const float4 LB = e + 1 < n ? qL[wid][e1] : make_float4(0.f, 0.f, 0.f, 0.f);
+                        const float4 GA = qG[wid][e], GB = qG[wid][e1];
+                        const unsigned ca = __float_as_uint(GA.z), cbv = __float_as_uint(GB.z);
+                        float XA[RPL + 1], XB[RPL + 1];
+#pragma unroll
+                        for (int r = 0; r < RPL; r++) {
+                            const float rowf = (float)(RPL * lane + r);
+                            const float2 gg = make_float2(__saturatef(fmaf(rowf, GA.x, GA.y)),
+                                                          __saturatef(fmaf(rowf, GB.x, GB.y)));
+                            const float2 ff = fma2(gg, bcast2(fnz), bcast2(-0.5f));
+                            const float2 rm = add2(ff, bcast2(12582912.0f));
+                            const float2 qa = __ldg(Q + (ca + __float_as_uint(rm.x)));
+                            const float2 qb = __ldg(Q + (cbv + __float_as_uint(rm.y)));
+                            XA[r] = fmaf(ff.x, qa.y, qa.x);
+                            XB[r] = fmaf(ff.y, qb.y, qb.x);
+                        }
+                        const float xa = __shfl_down_sync(0xffffffffu, XA[0], 1);
+                        const float xb = __shfl_down_sync(0xffffffffu, XB[0], 1);
+                        XA[RPL] = lane == 31 ? GA.w : xa;
+                        XB[RPL] = lane == 31 ? GB.w : xb;
+                        if (RPL >= 2) {
+#pragma unroll
+                            for (int r = 0; r + 1 < RPL; r += 2) {
+                                const float2 ra = make_float2(XA[r + 1] - XA[r], XA[r + 2] - XA[r + 1]);
+                                const float2 rb = make_float2(XB[r + 1] - XB[r], XB[r + 2] - XB[r + 1]);
+                                const float la[4] = {LA.x, LA.y, LA.z, LA.w}, lb[4] = {LB.x, LB.y, LB.z, LB.w};
+#pragma unroll
+                                for (int c = 0; c < F3_CPW; c++) {
+                                    float2 a2 = make_float2(acc[c][r], acc[c][r + 1]);
+                                    a2 = fma2(bcast2(la[c]), ra, a2);
+                                    a2 = fma2(bcast2(lb[c]), rb, a2);
+                                    acc[c][r] = a2.x;
+                                    acc[c][r + 1] = a2.y;
+                                }
+                            }
+                        } else {
+                            const float ra = XA[1] - XA[0], rb = XB[1] - XB[0];
+                            acc[0][0] = fmaf(LB.x, rb, fmaf(LA.x, ra, acc[0][0]));
+                            acc[1][0] = fmaf(LB.y, rb, fmaf(LA.y, ra, acc[1][0]));
+                            acc[2][0] = fmaf(LB.z, rb, fmaf(LA.z, ra, acc[2][0]));
+                            acc[3][0] = fmaf(LB.w, rb, fmaf(LA.w, ra, acc[3][0]));
+                        }
+                    }
+                }
+#pragma unroll (kF3SingleUnroll)
+                for (int e = 0; (!PFX || !F3_PAIRS) && e < n; e++) {
                     const float4 L4 = qL[wid][e];
                     const float4 q = qG[wid][e];
                     const int col = __float_as_int(q.z);
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
-                        // X(u) = H (A_k + f' x_k), A_k = P_k - (k - 1/2) x_k, f' = (u - B0)/H - 1/2,
-                        // k = round(f') (1.5*2^23 magic number; f' clamped to [-1/2, nz - 1/2],
-                        // where either rounding of a tie gives the same X: X is continuous and
-                        // Q_nz = (P_nz, 0)), at the lane's RPL lower row boundaries; the upper
-                        // boundary of its last row is the next lane's first (shuffle), lane 31
-                        // takes the producer's X(RPL*32).  Unsigned 32-bit element offsets.
-                        const unsigned cb2 = (unsigned)col * (unsigned)pfx_stride - 0x4B400000u;
+                        // one hit at a time (same arithmetic as the pair loop above)
+                        const unsigned cq = __float_as_uint(q.z);
                         float Xp[RPL + 1];
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
-                            float f = fmaf((float)(RPL * lane + r), q.y, q.x);
-                            f = fminf(fmaxf(f, -0.5f), fnz - 0.5f);
+                            const float g = __saturatef(fmaf((float)(RPL * lane + r), q.x, q.y));
+                            const float f = fmaf(g, fnz, -0.5f);
                             const float rm = __fadd_rn(f, 12582912.0f);
-                            const float2 qk = __ldg(Q + (cb2 + (unsigned)__float_as_int(rm)));
+                            const float2 qk = __ldg(Q + (cq + __float_as_uint(rm)));
                             Xp[r] = fmaf(f, qk.y, qk.x);
                         }
                         const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);

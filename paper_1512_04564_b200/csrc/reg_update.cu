@@ -61,16 +61,24 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
     const float xv = W[ZB][1][1];
     const float kj = KAPPA ? K[ZB][1][1] : 1.f;
     float gs = 0.f, cs = 0.f, cmax = 0.f;
+    // interior path: the two neighbours of a direction as one packed pair (FFMA2 / FMUL2), the
+    // sums kept per half and added at the end
+    float2 gs2 = make_float2(0.f, 0.f), cs2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int d = 0; d < NDIRS; d++) {
         const int ox = dir_x(d), oy = dir_y(d), oz = dir_z(d);
         const int zp = oz > 0 ? ZC : ZB, zm = oz > 0 ? ZA : ZB;
         if (!CHECK && !KAPPA) {
-            const float tp = xv - W[zp][1 + oy][1 + ox];
-            const float tm = xv - W[zm][1 - oy][1 - ox];
-            const float op = omega_scaled<POT>(tp, rp), om = omega_scaled<POT>(tm, rp);
-            gs = fmaf(rp.beta[d], fmaf(tp, op, tm * om), gs);
-            cs = fmaf(rp.beta[d], op + om, cs);
+            const float2 t = make_float2(xv - W[zp][1 + oy][1 + ox], xv - W[zm][1 - oy][1 - ox]);
+            float2 o;
+            if (POT == 1) {
+                const float2 u = fma2(t, t, bcast2(1.f));
+                o = make_float2(rsqrt_ftz(u.x), rsqrt_ftz(u.y));
+            } else {
+                o = make_float2(omega_scaled<POT>(t.x, rp), omega_scaled<POT>(t.y, rp));
+            }
+            gs2 = fma2(bcast2(rp.beta[d]), mul2(t, o), gs2);
+            cs2 = fma2(bcast2(rp.beta[d]), o, cs2);
         } else {
 #pragma unroll
             for (int sg = 0; sg < 2; sg++) {
@@ -89,6 +97,10 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
                 }
             }
         }
+    }
+    if (!CHECK && !KAPPA) {
+        gs = gs2.x + gs2.y;
+        cs = cs2.x + cs2.y;
     }
     gs_out = gs;
     // maximum curvature: omega(0) = 1 for every in-volume neighbour (interior, no kappa: bsum)
@@ -155,6 +167,9 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 //     the boundary layout (coalesced over i); with pfx the z-prefix of x+.
 //   UPD_STEN (ct_reg_grad, and the multi-GPU path where the stencil of the new
 //     x overlaps the zeta all-reduce): grad R(x) and D_R(x) only.
+#ifndef UPD_ZDIV
+#define UPD_ZDIV 24
+#endif
 #ifndef UPD_MINB
 #define UPD_MINB 3  // <= 80 registers: 3 blocks of 256 per SM
 #endif
@@ -194,7 +209,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     // Interior columns load the 3x3 block unconditionally from a clamped plane (a
     // plane outside the volume is never weighted: the stencil checks km/kp there).
     const int klo = A.halo_lo ? -1 : 0, khi = A.halo_hi ? G.nz : G.nz - 1;   // readable planes of x
-    const float* __restrict__ xlo = x + (long long)klo * (long long)nxy;       // plane klo (kappa: klo = 0)
+    const float* __restrict__ xlo = x + (long long)klo * (long long)nxy;       // plane klo (x and kappa)
     auto load_plane = [&](auto slot_c, int k) {
         constexpr int S = decltype(slot_c)::value;
         if (inxy) {
@@ -203,7 +218,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
             const int kc = min(max(k, klo), khi);
             const unsigned off = (unsigned)(kc - klo) * nxy + col - nx - 1u;
             const float* __restrict__ p = xlo + off;
-            const float* __restrict__ pk = KAPPA ? kappa + off : nullptr;
+            const float* __restrict__ pk = KAPPA ? kappa + (long long)klo * (long long)nxy + off : nullptr;
 #pragma unroll
             for (int dy = 0; dy < 3; dy++) {
 #pragma unroll
@@ -359,14 +374,9 @@ struct UpdShape {
     int nzc, cz, jpb;
     size_t smem;
 };
-static int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-
 static UpdShape upd_shape(const DGeom& G, bool pfx) {
     UpdShape u;
-    static const int zdiv = env_int("CTR_UPD_ZDIV", 24);  // tuning knob: voxels per z-chunk target
+    constexpr int zdiv = UPD_ZDIV;   // voxels per z-chunk target (tuning variants: -DUPD_ZDIV=n)
     u.nzc = std::min(8, std::max(1, G.nz / std::max(1, zdiv)));
     u.cz = (G.nz + u.nzc - 1) / u.nzc;
     u.nzc = (G.nz + u.cz - 1) / u.cz;
@@ -402,12 +412,14 @@ static void upd_select(const DGeom& G, const RegParams& rp, const Ctl* ctl, cons
 }
 
 void launch_reg(const DGeom& G, const RegParams& rp, const float* x, const float* kappa, float* grad, float* curv,
-                cudaStream_t s) {
+                cudaStream_t s, bool halo_lo, bool halo_hi) {
     UpdArgs A = {};
     A.xin = x;
     A.kappa = kappa;
     A.grad_out = grad;
     A.curv_out = curv;
+    A.halo_lo = halo_lo;
+    A.halo_hi = halo_hi;
     upd_select<UPD_STEN>(G, rp, nullptr, A, s);
     launches_add(1);
 }
@@ -431,8 +443,9 @@ void launch_update(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* x
 
 void launch_update_halo(const DGeom& G, const RegParams& rp, const Ctl* ctl, float* xa, float* xb, const float* dl,
                         float* g, float* ht, float box_lo, float box_hi, float* pfx, bool halo_lo, bool halo_hi,
-                        cudaStream_t s) {
+                        cudaStream_t s, const float* kappa) {
     UpdArgs A = {};
+    A.kappa = kappa;
     A.xa = xa;
     A.xb = xb;
     A.dl = dl;
@@ -511,7 +524,20 @@ __global__ void k_init_from_zeta(long long n, const float* __restrict__ zeta, fl
     }
 }
 
-__global__ void k_advance(Ctl* ctl) { ctl->k += 1; }
+__global__ void k_advance(Ctl* ctl, int n) {
+    if ((int)threadIdx.x < n) ctl[threadIdx.x].k += 1;
+}
+
+// dst[i] = src[0][i] + src[1][i] + ... + src[n-1][i], src[p] = base + p * stride, summed in rank
+// order (deterministic): the single-process emulation of the partial-gradient reduction
+__global__ void k_sum_partials(float* __restrict__ base, int n, long long stride, long long count) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        float acc = base[i];
+        for (int p = 1; p < n; p++) acc += __ldg(base + p * stride + i);
+        base[i] = acc;
+    }
+}
 
 __global__ void k_fill(float* p, long long n, float v) {
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n;
@@ -580,8 +606,12 @@ void launch_kappa_ratio(long long n, const float* a, const float* b, float* kapp
     k_kappa_ratio<<<grid_for(n), 256, 0, s>>>(n, a, b, kappa);
     launches_add(1);
 }
-void launch_advance(Ctl* ctl, cudaStream_t s) {
-    k_advance<<<1, 1, 0, s>>>(ctl);
+void launch_advance(Ctl* ctl, cudaStream_t s, int n) {
+    k_advance<<<1, 32, 0, s>>>(ctl, n);
+    launches_add(1);
+}
+void launch_sum_partials(float* base, int n, long long stride, long long count, cudaStream_t s) {
+    k_sum_partials<<<grid_for(count), 256, 0, s>>>(base, n, stride, count);
     launches_add(1);
 }
 void launch_state_h(const DGeom& G, const float* dl, const float* x, const float* ht, float* h, cudaStream_t s) {

@@ -12,8 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# CTR_LIB_PATH: load another build of the same library (tuning experiments only)
-LIB_PATH = os.environ.get("CTR_LIB_PATH") or os.path.join(_HERE, "libctrecon.so")
+LIB_PATH = os.path.join(_HERE, "libctrecon.so")   # scripts/kbench.py --lib points it at a tuning variant
 
 CT_OK, CT_E_SHAPE, CT_E_CONFIG, CT_E_NUMERIC, CT_E_DIVERGED, CT_E_CUDA, CT_E_NCCL, CT_E_NOMEM = range(8)
 STATUS_NAMES = ["CT_OK", "CT_E_SHAPE", "CT_E_CONFIG", "CT_E_NUMERIC", "CT_E_DIVERGED", "CT_E_CUDA",
@@ -71,7 +70,7 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
            "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
            "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size", "ct_forward_zprefix",
-           "oslalm_residual"]
+           "oslalm_residual", "ct_dist_create_local"]
 
 _lib = None
 
@@ -116,6 +115,7 @@ def load():
     L.ct_sino_upload.argtypes = [vp, vp, ct_views, vp, vp]
     L.ct_nccl_unique_id.argtypes = [P(ctypes.c_ubyte)]
     L.ct_dist_create.argtypes = [ctypes.c_int, ctypes.c_int, P(ctypes.c_ubyte), ctypes.c_int, P(vp)]
+    L.ct_dist_create_local.argtypes = [ctypes.c_int, ctypes.c_int, P(vp)]
     L.ct_dist_destroy.argtypes = [vp]
     L.ct_dist_destroy.restype = None
     L.ct_launch_count.restype = ctypes.c_int64
@@ -125,7 +125,7 @@ def load():
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
                  "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size",
-                 "ct_forward_zprefix", "oslalm_residual"):
+                 "ct_forward_zprefix", "oslalm_residual", "ct_dist_create_local"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -320,6 +320,13 @@ def ct_dist_create(rank, world, uid, device):
     buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
     h = ctypes.c_void_p()
     _check(load().ct_dist_create(int(rank), int(world), buf, int(device), ctypes.byref(h)))
+    return h
+
+
+def ct_dist_create_local(world, device=0):
+    """Single-process emulation of a `world`-rank view-sharded solve on one device."""
+    h = ctypes.c_void_p()
+    _check(load().ct_dist_create_local(int(world), int(device), ctypes.byref(h)))
     return h
 
 

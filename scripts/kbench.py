@@ -1,5 +1,5 @@
 """Per-kernel device times of one outer iteration (oslalm_profile) for a config.
-usage: python scripts/kbench.py [config] [reps]   (tuning knobs via CTR_* env vars)"""
+usage: python scripts/kbench.py [config] [reps] [--lib variants/name.so]  (a tuning variant of the library)"""
 import os
 import sys
 
@@ -13,8 +13,15 @@ from paper_1512_04564_b200 import ctrecon as C  # noqa: E402
 from paper_1512_04564_b200.recon import Recon  # noqa: E402
 from synth.configs import get_config  # noqa: E402
 
-cfg = get_config(sys.argv[1] if len(sys.argv) > 1 else "c4")
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+args = [a for a in sys.argv[1:]]
+lib = None
+if "--lib" in args:
+    i = args.index("--lib")
+    lib = args[i + 1]
+    del args[i:i + 2]
+    C.LIB_PATH = os.path.abspath(lib)
+cfg = get_config(args[0] if len(args) > 0 else "c4")
+reps = int(args[1]) if len(args) > 1 else 2
 inp = bench.make_inputs(cfg, "cuda")
 rec = Recon(cfg["geom"], inp["reg"], cfg["solver"], inp["y"], inp["w"], inp["x0"])
 rec.compute_DL()
@@ -22,5 +29,5 @@ M = cfg["solver"]["M"]
 rec.run(M)
 for r in range(reps):
     kms = C.oslalm_profile(rec.h, rec.y, rec.w, rec.reg, rec.kappa, rec.dl, rec.params, rec.state, M, rec.ws)
-    print("env=%s update %.4f fwd %.4f back %.4f ms/subiter" % (
-        {k: v for k, v in os.environ.items() if k.startswith("CTR_")}, kms[0] / M, kms[1] / M, kms[2] / M))
+    print("lib=%s update %.4f fwd %.4f back %.4f ms/subiter" % (
+        os.path.basename(C.LIB_PATH), kms[0] / M, kms[1] / M, kms[2] / M))

@@ -173,3 +173,103 @@ def test_zslab_gloo_partial_projections_and_halo_stencil(world):
         assert np.allclose(csl, cv[z0:z0 + n], rtol=1e-12, atol=1e-15)
         covered += n
     assert covered == g["nz"]
+
+
+def _owner_worker(rank, world, port, nsub, q):
+    """Algorithm 1 (oracle arithmetic) with the GPU dist path's data flow: views of each subset
+    sharded over the ranks, partial gradients reduced by z-slab to the slab owner (gloo reduce
+    per slab = the grouped ncclReduce / ncclReduceScatter), the owner's lines 7-8 and 4-5 on its
+    slab only, x+ re-assembled by a broadcast per owner (= ncclAllGather / grouped ncclBroadcast),
+    g and h gathered at the end of the call."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import alg
+        from oracle import projector as P
+        from tests.geoms import tiny
+        from tests.problems import oracle_problem, synthetic_problem
+        M, alpha = 3, 1.999
+        pb = synthetic_problem(tiny("helical_arc"), M=M)
+        prob = oracle_problem(pb)
+        g = pb["geom"]
+        nz, na = g["nz"], g["na"]
+        DL = pb["DL"]
+        slabs = [_slab(g, nz, r_, world)[:2] for r_ in range(world)]
+        z0, n = slabs[rank]
+        sl = slice(z0, z0 + n)
+
+        def partial_grad(x, m):
+            st, sd, cnt = shard_views(na, M, m, rank, world)
+            part = np.zeros(P.vol_shape(g))
+            if cnt > 0:
+                r = pb["w"][st::sd][:cnt] * (P.forward(g, x, (st, sd, cnt)) - pb["y"][st::sd][:cnt])
+                part = M * P.back(g, r, (st, sd, cnt))
+            return torch.from_numpy(part)
+
+        def reduce_to_owners(t):
+            for q_, (a, nn) in enumerate(slabs):
+                piece = t[a:a + nn].contiguous()
+                dist.reduce(piece, dst=q_)
+                if q_ == rank:
+                    t[a:a + nn] = piece
+            return t.numpy()
+
+        def gather_slabs(arr):
+            t = torch.from_numpy(np.ascontiguousarray(arr))
+            for q_, (a, nn) in enumerate(slabs):
+                piece = t[a:a + nn].contiguous()
+                dist.broadcast(piece, src=q_)
+                t[a:a + nn] = piece
+            return t.numpy()
+
+        x = pb["x0"].copy()
+        zeta = reduce_to_owners(partial_grad(x, M - 1))      # line 1 (reading R1), owners' slabs exact
+        zeta = gather_slabs(zeta)
+        gg, h = zeta.copy(), DL * x - zeta
+        k = 0
+        for _ in range(nsub):
+            m, rho = k % M, alg.rho_k(k, alpha)
+            gradR, DR = prob.reg(x)                            # x replicated: halos available
+            s = rho * (DL[sl] * x[sl] - h[sl]) + (1 - rho) * gg[sl]
+            xn = x.copy()
+            xn[sl] = alg._x_update(x[sl], s, gradR[sl], rho * DL[sl] + DR[sl])   # owner slab, lines 4-5
+            xn = gather_slabs(xn)
+            zeta = reduce_to_owners(partial_grad(xn, m))        # line 6, reduce-scatter
+            gg[sl] = rho / (rho + 1) * (alpha * zeta[sl] + (1 - alpha) * gg[sl]) + gg[sl] / (rho + 1)
+            h[sl] = alpha * (DL[sl] * xn[sl] - zeta[sl]) + (1 - alpha) * h[sl]
+            x = xn
+            k += 1
+        gg, h = gather_slabs(gg), gather_slabs(h)
+        if rank == 0:
+            q.put((x, gg, h))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("world", [2, 3])
+def test_owner_slab_data_flow_gloo_equals_algorithm1(world):
+    """The view-sharded path's data flow on `world` gloo ranks reproduces the
+    single-process Algorithm 1 iterates (equal slabs at world 2, nz = 10; unequal at world 3)."""
+    from oracle import alg
+    from tests.geoms import tiny
+    from tests.problems import oracle_problem, synthetic_problem
+    nsub = 5
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_owner_worker, args=(r, world, port, nsub, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    x, gg, h = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pb = synthetic_problem(tiny("helical_arc"), M=3)
+    prob = oracle_problem(pb)
+    trace = {}
+    alg.alg1(prob, pb["x0"], 3, 1.999, 2, DL=pb["DL"], trace=trace)
+    xo, go, ho = trace[nsub]
+    for a, b in ((x, xo), (gg, go), (h, ho)):
+        assert np.linalg.norm(a - b) <= 1e-10 * np.linalg.norm(b)

@@ -6,6 +6,9 @@ M > 1 on the BASELINE configs; its parts are pinned here:
        G^{1/2}, nu stays 0, for
        alpha in {1, 1.5, 1.999}, fixed rho and Eq. 37;
   P7b  alpha = 1: Alg. 1 == Alg. 2 == unrelaxed OS-LALM (PAPER.md:356);
+  P7d  Alg. 2 with M = 1 equals the literal Eq. 18 iteration (simple relaxation,
+       PAPER.md:142-155) for alpha in {1.5, 1.999} (the alpha-dependent
+       coefficients of its g recursion), fixed rho and Eq. 37;
   P7c  quadratic potential, M = 1: Alg. 1 converges to the dense PWLS
        minimiser (A'WA + H_R)^{-1}A'Wy; alpha = 1.999 gets there in fewer
        iterations than alpha = 1 (Theorem 2, PAPER.md:263);
@@ -126,6 +129,39 @@ def test_alg1_M1_equals_literal_eq25(alpha, rho_mode):
         assert np.all(nus[k] == 0.0)
     # the iteration moves (not a trivial fixed point)
     assert np.max(np.abs(xs_lit[-1] - xs_lit[0])) > 1e-4
+
+
+# ------------------------------------------------------------------ P7d
+@pytest.mark.parametrize("alpha", [1.5, 1.999])
+@pytest.mark.parametrize("rho_mode", ["fixed", "continuation"])
+def test_alg2_M1_equals_literal_eq18(alpha, rho_mode):
+    prob, x0, _ = tiny_problem("fan2d_arc", nx=8, ny=8, ns=16, na=12)
+    g = prob.g
+    DL = prob.D_L()
+    A = dense.dense_A(g)
+    sw = np.sqrt(prob.w.ravel())
+    Aw, yw = sw[:, None] * A, sw * prob.y.ravel()       # Eq. 36 substitution
+    n = 100
+    rhos = [0.3] * n if rho_mode == "fixed" else [alg.rho_k(k, alpha) for k in range(n)]
+
+    def psi_grad(x):
+        return prob.reg(x.reshape(P.vol_shape(g)))[0].ravel()
+
+    def psi_curv(x):
+        return prob.reg(x.reshape(P.vol_shape(g)))[1].ravel()
+
+    xs = dense.literal_eq18(Aw, yw, DL.ravel(), x0.ravel(), alpha, rhos, psi_grad, psi_curv)
+    scale = max(np.abs(xs[-1]).max(), 1.0)
+    for k in (1, 2, 3, 10, 50, n):
+        xa = alg.alg2(prob, x0, 1, alpha, k, DL=DL, rho_mode="continuation" if rho_mode != "fixed" else "fixed",
+                      rho_fixed=0.3)[0]
+        assert np.max(np.abs(xa.ravel() - xs[k])) <= 1e-10 * scale, k
+    # and the early iterates differ from the proposed method's (Alg. 1) at alpha > 1 (both reach the
+    # same fixed point later): the pin tells the two recursions apart
+    x1 = alg.alg1(prob, x0, 1, alpha, 3, DL=DL, rho_mode="continuation" if rho_mode != "fixed" else "fixed",
+                  rho_fixed=0.3)[0]
+    assert np.max(np.abs(x1.ravel() - xs[3])) > 1e-3 * np.max(np.abs(xs[3] - xs[0]))
+    assert np.max(np.abs(xs[-1] - xs[0])) > 1e-4
 
 
 # ------------------------------------------------------------------ P7b
