@@ -15,6 +15,25 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Device-side bounds checks for a debug build (-DCTR_DEBUG_CHECKS; compute-sanitizer is not
+// available on the GPU pool): every gather offset and shared-memory index the kernels compute
+// is checked against its array's extent, and a failure traps (the launch fails loudly).
+#ifdef CTR_DEBUG_CHECKS
+#include <cstdio>
+#define CTR_CHECK(cond, what)                                                                            \
+    do {                                                                                                 \
+        if (!(cond)) {                                                                                   \
+            printf("CTR_CHECK failed: %s (%s:%d) block (%d,%d,%d) thread (%d,%d,%d)\n", what, __FILE__,   \
+                   __LINE__, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, threadIdx.y, threadIdx.z);  \
+            __trap();                                                                                    \
+        }                                                                                                \
+    } while (0)
+#else
+#define CTR_CHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
+
 namespace ctr {
 
 constexpr int kMaxCells = 16;     // max detector columns under one voxel footprint

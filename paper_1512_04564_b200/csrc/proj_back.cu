@@ -113,6 +113,7 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
             const float wq = LZ ? F[q] * ray_Lz<ARC>(G, sw + q, tw + o) : F[q];
             rs = fmaf(wq, a[q], rs);
         }
+        CTR_CHECK(o < n, "back row buffer");
         cs[o * BK_BS] = make_float2(fmaf(ofs, rs, run), rs);
         run += rs;
         ofs -= 1.f;
@@ -238,6 +239,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
         for (int tw = t0; tw <= t1; tw += RM) {
             const int twe = min(t1, tw + RM - 1);
             const int n = twe - tw + 1;
+            CTR_CHECK(n >= 1 && n <= RM, "back rows per pass");
             float run = 0.f;
             const float* __restrict__ pr = proj + (pv + (unsigned)tw * (unsigned)G.ns + (unsigned)sw);
             if (W == 4) {
@@ -276,6 +278,9 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                                               __saturatef(fmaf((float)(q + 1), Hn, bn)));
                 const float2 vv = fma2(gg, bcast2(fn), bcast2(-0.5f));
                 const float2 rm = add2(vv, bcast2(12582912.0f));
+                CTR_CHECK(__float_as_int(rm.x) - 0x4B400000 >= 0 && __float_as_int(rm.x) - 0x4B400000 <= n &&
+                              __float_as_int(rm.y) - 0x4B400000 >= 0 && __float_as_int(rm.y) - 0x4B400000 <= n,
+                          "back boundary row");
                 const float2 ca = cs[(__float_as_int(rm.x) - 0x4B400000) * BK_BS];
                 const float2 cb = cs[(__float_as_int(rm.y) - 0x4B400000) * BK_BS];
                 return make_float2(fmaf(vv.x, ca.y, ca.x), fmaf(vv.y, cb.y, cb.x));

@@ -197,20 +197,18 @@ constexpr int F3_WARPS = F3_NWARPS;
 constexpr int F3_CPW = 4;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
-// Tuning experiment kept as a compile-time switch: consuming queued hits two at a
-// time in packed FP32 (FFMA2 / FADD2 across the pair) cuts the hit loop from ~33 to ~23.5
-// instructions per hit but ran slower (c4 fwd 2.72 ms unrolled 1, 3.00 ms unrolled 2, vs 2.51 ms
-// one hit at a time, r2d): the loop is bound by its prefix gathers, not by issue.
-#ifndef F3_PAIRS
-#define F3_PAIRS 0     // PFX: queued hits consumed two at a time in packed FP32
-#endif
-#ifndef F3_PUNROLL
-#define F3_PUNROLL 2   // pair-loop unroll
-#endif
 #ifndef F3_SUNROLL
-#define F3_SUNROLL 4   // single-hit loop unroll
+#define F3_SUNROLL 4   // hit-loop unroll
 #endif
-constexpr int kF3PairUnroll = F3_PUNROLL, kF3SingleUnroll = F3_SUNROLL;
+#ifndef F3_STRIDED
+#define F3_STRIDED 0   // lane l owns detector rows RPL l + r (0) or l + 32 r (1)
+#endif
+constexpr int kF3SingleUnroll = F3_SUNROLL;
+// Detector row r of lane l.  The strided assignment (l + 32 r: each gather instruction covers 32
+// consecutive rows, about half the cache lines of the consecutive one) measured slower (c4 fwd
+// 2.60 vs 2.51 ms, r2h) and is kept as a tuning switch only.
+template <int RPL>
+__device__ __forceinline__ int fwd_row(int lane, int r) { return F3_STRIDED ? lane + 32 * r : RPL * lane + r; }
 #ifndef F3_PREYW
 #define F3_PREYW 1     // epilogue y, w copied into shared memory by cp.async at kernel start
 #endif
@@ -365,6 +363,8 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         const float gt = __saturatef(fmaf((float)(RPL * 32), ih, bg));
                         ft = fmaf(gt, fnz, -0.5f);
                         const float rt = __fadd_rn(ft, 12582912.0f);
+                        CTR_CHECK((unsigned long long)(cbq + __float_as_uint(rt)) <
+                                      (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd top gather");
                         qt = __ldg(Q + (cbq + __float_as_uint(rt)));
                     }
                     if (cand) {
@@ -394,97 +394,57 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 const int n = __popc(m);
                 if (nz) {
                     const int slot = __popc(m & lanemask_lt);
+                    CTR_CHECK(slot < 32, "fwd queue slot");
                     qL[wid][slot] = eL;
                     qG[wid][slot] = eG;
                 }
                 __syncwarp();
-                if (PFX && F3_PAIRS) {
-                    // Two queued voxel columns A, B at a time, packed FP32 (FFMA2 / FADD2) across them:
-                    // X(u) = A_k + f x_k (A_k = P_k - (k - 1/2) x_k, f the clamped voxel coordinate
-                    // minus 1/2, k = round(f) by the 1.5 2^23 magic number; either rounding of a tie
-                    // gives the same X: X is continuous and Q_nz = (P_nz, 0)) at the lane's RPL lower
-                    // row boundaries; the upper boundary of its last row is the next lane's first
-                    // (shuffle), lane 31 takes the producer's X(RPL 32).  Row sums Rs = X(t+1) - X(t)
-                    // times H (folded into L) are credited to the four detector columns two rows at a
-                    // time (FFMA2 with the column weight broadcast).  Unsigned 32-bit element offsets.
-#pragma unroll (kF3PairUnroll)
-                    for (int e = 0; e < n; e += 2) {
-                        // an odd count: the last pair repeats the last hit with zero weight (its
-                        // gathers hit the lines the first half just fetched)
-                        const int e1 = min(e + 1, n - 1);
-                        const float4 LA = qL[wid][e];
-                        const float4 LB = e + 1 < n ? qL[wid][e1] : make_float4(0.f, 0.f, 0.f, 0.f);
-                        const float4 GA = qG[wid][e], GB = qG[wid][e1];
-                        const unsigned ca = __float_as_uint(GA.z), cbv = __float_as_uint(GB.z);
-                        float XA[RPL + 1], XB[RPL + 1];
-#pragma unroll
-                        for (int r = 0; r < RPL; r++) {
-                            const float rowf = (float)(RPL * lane + r);
-                            const float2 gg = make_float2(__saturatef(fmaf(rowf, GA.x, GA.y)),
-                                                          __saturatef(fmaf(rowf, GB.x, GB.y)));
-                            const float2 ff = fma2(gg, bcast2(fnz), bcast2(-0.5f));
-                            const float2 rm = add2(ff, bcast2(12582912.0f));
-                            const float2 qa = __ldg(Q + (ca + __float_as_uint(rm.x)));
-                            const float2 qb = __ldg(Q + (cbv + __float_as_uint(rm.y)));
-                            XA[r] = fmaf(ff.x, qa.y, qa.x);
-                            XB[r] = fmaf(ff.y, qb.y, qb.x);
-                        }
-                        const float xa = __shfl_down_sync(0xffffffffu, XA[0], 1);
-                        const float xb = __shfl_down_sync(0xffffffffu, XB[0], 1);
-                        XA[RPL] = lane == 31 ? GA.w : xa;
-                        XB[RPL] = lane == 31 ? GB.w : xb;
-                        if (RPL >= 2) {
-#pragma unroll
-                            for (int r = 0; r + 1 < RPL; r += 2) {
-                                const float2 ra = make_float2(XA[r + 1] - XA[r], XA[r + 2] - XA[r + 1]);
-                                const float2 rb = make_float2(XB[r + 1] - XB[r], XB[r + 2] - XB[r + 1]);
-                                const float la[4] = {LA.x, LA.y, LA.z, LA.w}, lb[4] = {LB.x, LB.y, LB.z, LB.w};
-#pragma unroll
-                                for (int c = 0; c < F3_CPW; c++) {
-                                    float2 a2 = make_float2(acc[c][r], acc[c][r + 1]);
-                                    a2 = fma2(bcast2(la[c]), ra, a2);
-                                    a2 = fma2(bcast2(lb[c]), rb, a2);
-                                    acc[c][r] = a2.x;
-                                    acc[c][r + 1] = a2.y;
-                                }
-                            }
-                        } else {
-                            const float ra = XA[1] - XA[0], rb = XB[1] - XB[0];
-                            acc[0][0] = fmaf(LB.x, rb, fmaf(LA.x, ra, acc[0][0]));
-                            acc[1][0] = fmaf(LB.y, rb, fmaf(LA.y, ra, acc[1][0]));
-                            acc[2][0] = fmaf(LB.z, rb, fmaf(LA.z, ra, acc[2][0]));
-                            acc[3][0] = fmaf(LB.w, rb, fmaf(LA.w, ra, acc[3][0]));
-                        }
-                    }
-                }
 #pragma unroll (kF3SingleUnroll)
-                for (int e = 0; (!PFX || !F3_PAIRS) && e < n; e++) {
+                for (int e = 0; e < n; e++) {
                     const float4 L4 = qL[wid][e];
                     const float4 q = qG[wid][e];
                     const int col = __float_as_int(q.z);
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
-                        // one hit at a time (same arithmetic as the pair loop above)
+                        // X(u) = A_k + f x_k (A_k = P_k - (k - 1/2) x_k; f the voxel coordinate
+                        // minus 1/2 of row boundary u, clamped to [-1/2, nz - 1/2] as f = nz g - 1/2
+                        // with g = sat(u ih + bg); k = round(f) by the 1.5 2^23 magic number, either
+                        // rounding of a tie giving the same X: X is continuous and Q_nz = (P_nz, 0))
+                        // at the lower boundary of each of the lane's rows; the upper boundary of a
+                        // row is the next row's lower one (the next lane's, by a rotation shuffle;
+                        // lane 31 takes lane 0's next row, or the producer's X at the top).
+                        // Unsigned 32-bit element offsets.
                         const unsigned cq = __float_as_uint(q.z);
-                        float Xp[RPL + 1];
+                        float Xp[RPL];
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
-                            const float g = __saturatef(fmaf((float)(RPL * lane + r), q.x, q.y));
+                            const float g = __saturatef(fmaf((float)fwd_row<RPL>(lane, r), q.x, q.y));
                             const float f = fmaf(g, fnz, -0.5f);
                             const float rm = __fadd_rn(f, 12582912.0f);
+                            CTR_CHECK((unsigned long long)(cq + __float_as_uint(rm)) <
+                                          (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd prefix gather");
                             const float2 qk = __ldg(Q + (cq + __float_as_uint(rm)));
                             Xp[r] = fmaf(f, qk.y, qk.x);
                         }
-                        const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);
-                        Xp[RPL] = lane == 31 ? q.w : xn;
+                        if (F3_STRIDED) {
+                            float v[RPL];
 #pragma unroll
-                        for (int r = 0; r < RPL; r++) Rs[r] = Xp[r + 1] - Xp[r];
+                            for (int r = 0; r < RPL; r++) v[r] = __shfl_sync(0xffffffffu, Xp[r], (lane + 1) & 31);
+#pragma unroll
+                            for (int r = 0; r < RPL; r++)
+                                Rs[r] = (lane < 31 ? v[r] : (r + 1 < RPL ? v[(r + 1) % RPL] : q.w)) - Xp[r];
+                        } else {
+                            const float xn = __shfl_down_sync(0xffffffffu, Xp[0], 1);
+#pragma unroll
+                            for (int r = 0; r < RPL; r++)
+                                Rs[r] = (r + 1 < RPL ? Xp[(r + 1) % RPL] : (lane == 31 ? q.w : xn)) - Xp[r];
+                        }
                     } else {
                         const float* __restrict__ xc = x + col;
                         const float btop = fmaf(fnz, q.y, q.x);
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
-                            const int t = RPL * lane + r;
+                            const int t = fwd_row<RPL>(lane, r);
                             const float tb = (float)t, tb1 = (float)(t + 1);
                             float a = 0.f;
                             if (t < G.nt && tb1 > q.x && tb < btop) {
@@ -496,6 +456,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                                     if (bk >= tb1) break;
                                     const float bk1 = fmaf((float)(k + 1), q.y, q.x);
                                     const float ov = fminf(bk1, tb1) - fmaxf(bk, tb);
+                                    CTR_CHECK(k >= 0 && k < G.nz, "fwd direct z index");
                                     if (ov > 0.f) a = fmaf(ov, ONES ? 1.f : __ldg(&xc[(size_t)k * G.nxy]), a);
                                     bk = bk1;
                                 }
@@ -520,7 +481,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #pragma unroll
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
-        for (int r = 0; r < RPL; r++) stage[RPL * lane + r][wid * F3_CPW + c] = acc[c][r];
+        for (int r = 0; r < RPL; r++) stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c] = acc[c][r];
 #if F3_PREYW
     if (YW) asm volatile("cp.async.wait_all;" ::: "memory");
 #endif
@@ -530,6 +491,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         const int ss = sb0 + c;
         if (ss >= G.ns) continue;
         const float lz = ray_Lz<ARC>(G, ss, t);
+        CTR_CHECK(t < 32 * RPL, "fwd stage row");
         const float p = lz * stage[t][c];
         const size_t o = ((size_t)vi * G.nt + t) * G.ns + ss;
         if (MODE == FWD_PLAIN) {

@@ -137,6 +137,7 @@ enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
 // [k - 1/2, k + 1/2] is then one FFMA, A_k + f x_k.
 __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__ pfx, const float* xs, float* tot,
                                              float run, int c, int lane, bool act, unsigned col, int k0, int k1) {
+    CTR_CHECK(c < (int)blockDim.y && k1 <= G.nz, "update prefix chunk");
     tot[c * 32 + lane] = run;
     // only the NZC chunk-warps of this row exchange totals (xs is per thread): a named
     // barrier per row instead of the whole block
@@ -217,6 +218,8 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
             // -1 of a z-slab lies below x); (kc - klo) * nxy + col - nx - 1 < 2^32
             const int kc = min(max(k, klo), khi);
             const unsigned off = (unsigned)(kc - klo) * nxy + col - nx - 1u;
+            CTR_CHECK(col >= nx + 1u && (unsigned long long)(kc - klo) * nxy + col + nx + 1u <
+                                            (unsigned long long)(khi - klo + 1) * nxy, "update window");
             const float* __restrict__ p = xlo + off;
             const float* __restrict__ pk = KAPPA ? kappa + (long long)klo * (long long)nxy + off : nullptr;
 #pragma unroll
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
             }
         }
         if (FULL && A.pfx) {
+            CTR_CHECK(k >= 0 && k < G.nz, "update prefix staging");
             xs[k * 33 + lane] = xnew;
             run += xnew;
         }
