@@ -257,18 +257,26 @@ def run_reference(args):
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     inputs = make_inputs(cfg, dev)
     M = cfg["solver"]["M"]
-    # each step: a bounded sample of one sub-iteration (oracle_sample), sized so that the whole
-    # --steps/--warmup run takes ~150 s of oracle work; value = the mean of the extrapolated rates
-    state = _oracle_state(cfg, inputs)
+    # each step: one whole sub-iteration of the oracle (oracle.alg.alg1_run) when it fits the budget
+    # (~150 s of oracle work over the --steps/--warmup run), else a bounded sample of it
+    # (oracle_sample, views spread over the subset) sized to the budget; value = steps / total seconds
     budget = 150.0 / max(1, args.steps + args.warmup)
-    est, _ = oracle_sample(cfg, inputs, 0.02, state=state)   # probe (2% of a sub-iteration)
-    frac = min(1.0, budget / max(est, 1e-9))
-    for _ in range(args.warmup):
-        oracle_sample(cfg, inputs, frac, state=state)
+    t_full = oracle_full_subiter(cfg, inputs)          # first warm-up step, and the size probe
     ests = []
-    for _ in range(args.steps):
-        e, sample = oracle_sample(cfg, inputs, frac, state=state)
-        ests.append(e)
+    if t_full <= budget:
+        for _ in range(args.warmup - 1):
+            oracle_full_subiter(cfg, inputs)
+        for _ in range(args.steps):
+            ests.append(oracle_full_subiter(cfg, inputs))
+        sample = "one whole sub-iteration (Alg. 1 lines 4-9, oracle.alg.alg1_run, subset 5 of %d)" % M
+    else:
+        state = _oracle_state(cfg, inputs)
+        frac = min(1.0, budget / t_full)
+        for _ in range(args.warmup - 1):
+            oracle_sample(cfg, inputs, frac, state=state)
+        for _ in range(args.steps):
+            e, sample = oracle_sample(cfg, inputs, frac, state=state)
+            ests.append(e)
     val = len(ests) / sum(ests)
     cores = P.max_threads()
     line = {"impl": "reference", "metric": "relaxed OS-LALM subset-iters/s", "value": val,

@@ -4,6 +4,7 @@
 // and the NCCL view-sharded path.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cmath>
@@ -50,6 +51,12 @@ static ct_status fail(ct_status st, const char* fmt, ...) {
         ncclResult_t r_ = (call);                                                            \
         if (r_ != ncclSuccess) return fail(CT_E_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
     } while (0)
+
+// NVTX range for the duration of a scope (profiler timelines; no cost without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ handles
 struct GraphKey {
@@ -321,6 +328,7 @@ extern "C" ct_status ct_sqs_diag(const ct_geom* g, const float* w, const ct_dist
     int chunk = (int)std::min<size_t>(workspace_bytes / per_view, 65535);
     if (chunk < 1) return fail(CT_E_NOMEM, "ct_sqs_diag: workspace %zu < %zu bytes", workspace_bytes, per_view);
     DeviceGuard guard(g->device);
+    NvtxRange nv("ct_sqs_diag");
     cudaStream_t cs = (cudaStream_t)s;
     const int world = dist ? dist->world : 1;
     CT_CUDA(cudaMemsetAsync(d_out, 0, sizeof(float) * g->G.nvox, cs));
@@ -560,8 +568,11 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     // pageable source: the copy is staged before cudaMemcpyAsync returns
     CT_CUDA(cudaMemcpyAsync(ctl, hctl.data(), sizeof(Ctl) * nl, cudaMemcpyHostToDevice, s));
 
+    NvtxRange nv_solve(dist ? (dist->local ? "oslalm_relaxed_solve (local ranks)" : "oslalm_relaxed_solve (NCCL)")
+                             : "oslalm_relaxed_solve");
     // ---- line 1: rho = 1, zeta = g = M grad L_M(x), h = D_L x - zeta  (htilde = zeta)
     if (st->k == 0) {
+        NvtxRange nv1("Algorithm 1 line 1");
         float* zdst = dist ? zeta : st->g;
         // every local rank's partial gradient is accumulated in rank order into zdst
         bool first = true;

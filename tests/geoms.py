@@ -50,7 +50,9 @@ def mid(kind, **over):
                     the last ragged; two update z-chunks with the per-row prefix exchange),
                     H = 1.4-2.4 rows per voxel (24-voxel chunks span 34-58 rows: two
                     40-row passes in the back-projector)
-      helical_rpl4  flat, nt = 96 (four rows per lane), 4-warp forward over all views
+      helical_rpl4  flat, nt = 96 (four rows per lane), 4-warp forward over all views, nz = 80
+                    (four 24-voxel z-chunks, the last ragged: the back-projector's chunks share
+                    each column's footprint)
       axial_mid     flat axial, nt = 40, nz = 50 (two update z-chunks)"""
     if kind == "helical_mid":
         g = _geom(dim=3, nx=36, ny=36, nz=56, dx=1.0, dy=1.0, dz=1.0, det="arc", ns=160, nt=64,
@@ -58,7 +60,7 @@ def mid(kind, **over):
                   orbit_deg=720.0, pitch=1.0)
         g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 1.0, 720.0)
     elif kind == "helical_rpl4":
-        g = _geom(dim=3, nx=32, ny=30, nz=60, dx=1.0, dy=1.0, dz=0.8, det="flat", ns=128, nt=96,
+        g = _geom(dim=3, nx=32, ny=30, nz=80, dx=1.0, dy=1.0, dz=0.8, det="flat", ns=128, nt=96,
                   ds=0.7, dt=0.8, offset_s=-0.6, offset_t=0.4, dso=100.0, dsd=180.0, na=300,
                   orbit_deg=720.0, pitch=0.9, orbit_start_deg=5.0)
         g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 0.9, 720.0)
