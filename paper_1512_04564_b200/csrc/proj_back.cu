@@ -138,9 +138,9 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
 //      piecewise-linear cumulative R(u) = A_o + v rs_o, A_o = cs_o - (o - 1/2) rs_o
 //      (one 8-byte shared load and one FFMA per voxel boundary, magic-number
 //      rounding).
-template <bool ARC, int EPI, bool LZ, int BK_KZ, bool SHARE>
+template <bool ARC, int EPI, bool LZ, int BK_KZ>
 #ifndef BK_VSM
-#define BK_VSM 120     // view descriptors of the block's window staged in shared memory
+#define BK_VSM 128     // view descriptors of the block's window staged in shared memory
 #endif
 #ifndef BK_EPB
 #define BK_EPB 12      // voxels per batch of the g/htilde epilogue (loads of a batch issued together)
@@ -155,24 +155,15 @@ __global__ void __launch_bounds__(BK_BS, BK_KZ <= 16 ? 7 : BK_KZ <= 24 ? BK_MINB
 k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
-    // SHARE keeps 5 blocks per SM with its footprint arrays by buffering 4 rows fewer per pass
-    constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : BK_KZ <= 24 ? (SHARE ? BK_RM24 - 4 : BK_RM24) : 44;
+    constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : BK_KZ <= 24 ? BK_RM24 : 44;
     __shared__ float2 csb[RM + 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    const int lane = threadIdx.x;
     const int i = blockIdx.x * 32 + threadIdx.x;
-    // SHARE: the block's BK_Y warps are BK_Y z-chunks of the same 32 voxel columns and share each
-    // (column, view) transaxial footprint (computed by one warp per view, shared memory);
-    // otherwise the warps are BK_Y rows j of one z-chunk
-    const int j = SHARE ? blockIdx.y : blockIdx.y * BK_Y + threadIdx.y;
-    const int k0 = SHARE ? (blockIdx.z * BK_Y + threadIdx.y) * BK_KZ : blockIdx.z * BK_KZ;
+    const int j = blockIdx.y * BK_Y + threadIdx.y;
+    const int k0 = blockIdx.z * BK_KZ;
     const Views V = select_views(ctl, vsel);
     const int nt = G.nt;
-    const float fkz = (float)max(0, min(BK_KZ, G.nz - k0));
-    const bool act = i < G.nx && j < G.ny && k0 < G.nz;
-    // z-range whose views the block visits (SHARE: all of its chunks)
-    const int kb0 = SHARE ? blockIdx.z * BK_Y * BK_KZ : k0;
-    const float fkb = SHARE ? (float)min(BK_Y * BK_KZ, G.nz - kb0) : fkz;
+    const float fkz = (float)min(BK_KZ, G.nz - k0);
 
     // Helical view window of the block's z-chunk: the chunk [zlo, zhi] can reach the
     // detector rows [0, nt) only if zlo - (nt - tc)/m < z_s < zhi + tc/m for some
@@ -182,7 +173,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     int vi0 = 0, vi1 = V.count;
     if (G.zstep != 0.f && V.count > 0) {
         const float mlo = G.dsd / (G.dso + G.rxy) * G.inv_dt, mhi = G.dsd / (G.dso - G.rxy) * G.inv_dt;
-        const float zlo = G.zbot + (float)kb0 * G.dz, zhi = zlo + fkb * G.dz;
+        const float zlo = G.zbot + (float)k0 * G.dz, zhi = zlo + fkz * G.dz;
         const float up = (float)nt - G.t_c0p;   // rows above / below the row of z = z_s
         const float wlo = zlo - fmaxf(up / mlo, up / mhi) - 1.f;
         const float whi = zhi + fmaxf(G.t_c0p / mlo, G.t_c0p / mhi) + 1.f;
@@ -199,113 +190,39 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     const int nstage = max(0, min(vi1 - vi0, BK_VSM));
     for (int q = tid; q < nstage; q += BK_BS) vsm[q] = __ldg(&vtab[V.start + (vi0 + q) * V.stride]);
     __syncthreads();
-    if (!SHARE && !act) return;
+    if (i >= G.nx || j >= G.ny) return;
     float2* __restrict__ cs = &csb[0][tid];
 
     float acc[BK_KZ];
 #pragma unroll
     for (int q = 0; q < BK_KZ; q++) acc[q] = 0.f;
 
-    // SHARE: per group of BK_Y views, warp y computes the footprint of view vg + y for the block's
-    // 32 columns into shared memory; then every warp (z-chunk) back-projects the group's views
-    constexpr int NFP = SHARE ? BK_Y : 1;
-    __shared__ float fpF[NFP][BK_WMAX][32];          // F1 L_xy of the window's columns
-    __shared__ float4 fpA[NFP][32];                  // (B0, H or -1 if idle, -, slo | nc << 16 as float bits)
-    __shared__ int fpW[NFP];                         // window: 4, BK_WMAX, 0 (general: recomputed), -1 (view idle)
-    for (int vg = vi0; vg < vi1; vg += NFP) {
-      if (SHARE) {
-        const int vp = vg + (int)threadIdx.y;
-        bool ok = false;
-        Footprint f;
-        int slo = 0, nc = 0;
-        float B0 = 0.f, H = 0.f;
-        if (vp < vi1) {
-            const float4 vw = vp - vi0 < BK_VSM ? vsm[vp - vi0] : __ldg(&vtab[V.start + vp * V.stride]);
-            FpBase fb;
-            fp_base(G, vw.x, vw.y, i, j, fb);
-            fp_axial<ARC>(G, fb, vw.z, B0, H);
-            // any chunk of the block reaches the detector rows
-            const float clo = fmaf((float)kb0, H, B0), chi = fmaf(fkb, H, clo);
-            ok = i < G.nx && j < G.ny && clo < (float)nt && chi > 0.f;
-            if (ok) {
-                fp_trans<ARC>(G, vw.x, vw.y, fb, f);
-                slo = max((int)floorf(f.sfc + f.u0 + 0.5f), 0);
-                const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), G.ns - 1);
-                nc = shi - slo + 1;
-                ok = nc > 0;
-            }
-        }
-        const int ncmax = __reduce_max_sync(0xffffffffu, ok ? nc : 0);
-        const int W = ncmax <= 0 ? -1 : (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= BK_WMAX && G.ns >= BK_WMAX) ? BK_WMAX : 0;
-        const int sw = W > 0 ? max(min(slo, G.ns - W), 0) : slo;
-        const int y = threadIdx.y;
-        if (ok) {
-            float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
-#pragma unroll
-            for (int q = 0; q < BK_WMAX; q++) {
-                float Fq = 0.f;
-                if (q < 4 || q < W) {
-                    const float Tn = trap_T(f, ((float)(sw + q) + 0.5f) - f.sfc);
-                    Fq = (Tn - Tprev) * f.lxy;
-                    Tprev = Tn;
-                }
-                fpF[y][q][lane] = Fq;
-            }
-        }
-        fpA[y][lane] = make_float4(B0, ok ? H : -1.f, 0.f, __int_as_float(slo | (nc << 16)));
-        if (lane == 0) fpW[y] = W;
-        __syncthreads();
-      }
-      for (int v = 0; v < NFP; v++) {
-        const int vi = vg + v;
-        if (SHARE && (vi >= vi1 || !act)) break;
+    for (int vi = vi0; vi < vi1; vi++) {
+        const float4 vw = vi - vi0 < BK_VSM ? vsm[vi - vi0] : __ldg(&vtab[V.start + vi * V.stride]);
         FpBase fb;
-        float4 vw = make_float4(0.f, 0.f, 0.f, 0.f);
+        fp_base(G, vw.x, vw.y, i, j, fb);
         float B0, H;
-        if (SHARE) {
-            const float4 a = fpA[v][lane];
-            B0 = a.x;
-            H = a.y;
-            if (H < 0.f) continue;   // the column misses the detector in this view
-        } else {
-            vw = vi - vi0 < BK_VSM ? vsm[vi - vi0] : __ldg(&vtab[V.start + vi * V.stride]);
-            fp_base(G, vw.x, vw.y, i, j, fb);
-            fp_axial<ARC>(G, fb, vw.z, B0, H);
-        }
+        fp_axial<ARC>(G, fb, vw.z, B0, H);
         const float clo = fmaf((float)k0, H, B0);
         const float chi = fmaf(fkz, H, clo);
         const int t0 = max((int)floorf(clo), 0);
         const int t1 = min((int)ceilf(chi), nt) - 1;
         if (t0 > t1) continue;
         Footprint f;
-        int slo, nc, W, sw;
+        fp_trans<ARC>(G, vw.x, vw.y, fb, f);
+        // detector columns under the footprint
+        const int slo = max((int)floorf(f.sfc + f.u0 + 0.5f), 0);
+        const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), G.ns - 1);
+        const int nc = shi - slo + 1;
+        if (nc <= 0) continue;
+        const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
+        // warp-uniform window of W = 4 or BK_WMAX detector columns [sw, sw + W - 1] inside the
+        // detector (F1 is exactly 0 outside [u0, u3]); wider footprints take a general loop
+        const int ncmax = __reduce_max_sync(__activemask(), nc);
+        const int W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= BK_WMAX && G.ns >= BK_WMAX) ? BK_WMAX : 0;
+        const int sw = W ? max(min(slo, G.ns - W), 0) : slo;
         float F[BK_WMAX];
-        if (SHARE) {
-            W = fpW[v];
-            const float4 a = fpA[v][lane];
-            const int sn = __float_as_int(a.w);
-            slo = sn & 0xffff;
-            nc = sn >> 16;
-            sw = W > 0 ? max(min(slo, G.ns - W), 0) : slo;
-#pragma unroll
-            for (int q = 0; q < BK_WMAX; q++) F[q] = fpF[v][q][lane];
-            if (W == 0) {   // wide footprints (general loop below): the footprint again, locally
-                vw = vi - vi0 < BK_VSM ? vsm[vi - vi0] : __ldg(&vtab[V.start + vi * V.stride]);
-                fp_base(G, vw.x, vw.y, i, j, fb);
-                fp_trans<ARC>(G, vw.x, vw.y, fb, f);
-            }
-        } else {
-            fp_trans<ARC>(G, vw.x, vw.y, fb, f);
-            // detector columns under the footprint
-            slo = max((int)floorf(f.sfc + f.u0 + 0.5f), 0);
-            const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), G.ns - 1);
-            nc = shi - slo + 1;
-            if (nc <= 0) continue;
-            // warp-uniform window of W = 4 or BK_WMAX detector columns [sw, sw + W - 1] inside the
-            // detector (F1 is exactly 0 outside [u0, u3]); wider footprints take a general loop
-            const int ncmax = __reduce_max_sync(__activemask(), nc);
-            W = (ncmax <= 4 && G.ns >= 4) ? 4 : (ncmax <= BK_WMAX && G.ns >= BK_WMAX) ? BK_WMAX : 0;
-            sw = W ? max(min(slo, G.ns - W), 0) : slo;
+        {
             float Tprev = trap_T(f, ((float)sw - 0.5f) - f.sfc);
 #pragma unroll
             for (int q = 0; q < BK_WMAX; q++) {
@@ -318,7 +235,6 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 }
             }
         }
-        const unsigned pv = (unsigned)(vi * nt) * (unsigned)G.ns;  // < 2^32 (checked at launch)
         const float Bs = B0 - 0.5f;  // voxel boundary in row units minus (row + 1/2) below
         for (int tw = t0; tw <= t1; tw += RM) {
             const int twe = min(t1, tw + RM - 1);
@@ -386,12 +302,9 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 Rlo = Rh.y;
             }
         }
-      }
-      if (SHARE) __syncthreads();
     }
 
     // epilogue
-    if (SHARE && !act) return;
     const int kz = min(BK_KZ, G.nz - k0);
     if (EPI == BK_UPDATE) {
         // lines 7-8: g and htilde of the chunk in batches of EB voxels, every load of a batch
@@ -442,44 +355,27 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     }
 }
 
-// Experiment kept as a switch: blocks of BK_Y z-chunks of the same 32 columns that
-// compute each (column, view) footprint once, by one warp per view, and share it through shared
-// memory (one barrier pair per BK_Y views).  Correct (it passed the GPU suite, r2j) but 1.7x slower
-// (c4 back 4.03 vs 2.33 ms, c5 22.5 vs 13.4 ms): the barriers serialise the warps of a block and its
-// warps no longer read neighbouring rows j of the same detector rows (the L1 reuse of the default).
-#ifndef BK_SHARE
-#define BK_SHARE 0     // z-chunks of a block share each (column, view) footprint when the volume has >= BK_Y chunks
-#endif
-template <bool ARC, int KZ, bool SH>
-static void back3_launch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj, float scale,
-                         int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
-    dim3 block(32, BK_Y);
-    const int nch = (G.nz + KZ - 1) / KZ;
-    dim3 grid((G.nx + 31) / 32, SH ? G.ny : (G.ny + BK_Y - 1) / BK_Y, SH ? (nch + BK_Y - 1) / BK_Y : nch);
-    switch (epi) {
-        case BK_WRITE:
-            if (lz) k_back3<ARC, BK_WRITE, true, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back3<ARC, BK_WRITE, false, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        case BK_ACCUM:
-            if (lz) k_back3<ARC, BK_ACCUM, true, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back3<ARC, BK_ACCUM, false, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        case BK_INIT:
-            k_back3<ARC, BK_INIT, false, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-        default:
-            k_back3<ARC, BK_UPDATE, false, KZ, SH><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            break;
-    }
-}
-
 template <bool ARC, int KZ>
 static void back3_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,
                               float scale, int epi, bool lz, float* out, float* g, float* ht, cudaStream_t s) {
-    const int nch = (G.nz + KZ - 1) / KZ;
-    if (BK_SHARE && nch >= BK_Y) back3_launch<ARC, KZ, true>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s);
-    else back3_launch<ARC, KZ, false>(G, vtab, ctl, v, proj, scale, epi, lz, out, g, ht, s);
+    dim3 block(32, BK_Y);
+    dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, (G.nz + KZ - 1) / KZ);
+    switch (epi) {
+        case BK_WRITE:
+            if (lz) k_back3<ARC, BK_WRITE, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back3<ARC, BK_WRITE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_ACCUM:
+            if (lz) k_back3<ARC, BK_ACCUM, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            else k_back3<ARC, BK_ACCUM, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        case BK_INIT:
+            k_back3<ARC, BK_INIT, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+        default:
+            k_back3<ARC, BK_UPDATE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            break;
+    }
 }
 
 template <bool ARC>
@@ -520,6 +416,9 @@ static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, V
 #ifndef BK_KZSEL
 #define BK_KZSEL 24    // voxels per thread in z (tuning variants: -DBK_KZSEL=8 | 16 | 32)
 #endif
+// A variant with blocks of 4 z-chunks of the same 32 columns sharing each (column, view)
+// footprint through shared memory (one warp per view computes it, a barrier pair per 4 views) was
+// correct but 1.7x slower (c4 4.03 vs 2.33 ms; code in commit eb51f47).
 
 template <bool ARC, int DIM>
 static void back_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* proj,

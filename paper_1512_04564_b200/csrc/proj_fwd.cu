@@ -11,6 +11,7 @@
 //   FWD_RESID  r = L_z w (L_z q - y)     -> back-projector needs no L_z
 //   FWD_ONES_W r = L_z w (L_z A0 1)      (D_L = A'WA1)
 #include <algorithm>
+#include <cmath>
 
 #include "kernels.cuh"
 
@@ -197,6 +198,40 @@ constexpr int F3_WARPS = F3_NWARPS;
 constexpr int F3_CPW = 4;
 constexpr int F3_CPB = F3_WARPS * F3_CPW;   // detector columns per block
 
+// Experiment: F3_TMA = 1 stages each queued hit's run of z-prefix entries in shared
+// memory with a 1-D bulk copy (cp.async.bulk, the TMA engine) F3_TMAD hits ahead, completion
+// signalled on a per-slot mbarrier; the hit loop then reads the run from shared memory instead
+// of gathering from L2 / HBM.
+#ifndef F3_TMA
+#define F3_TMA 0
+#endif
+#ifndef F3_TMAD
+#define F3_TMAD 3      // bulk-copy ring depth (hits in flight per warp)
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned ok = 0;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+    } while (!ok);
+}
+// one lane: copy `bytes` (multiple of 16, both addresses 16-byte aligned) from global to shared,
+// completion counted on the barrier
+__device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 #ifndef F3_SUNROLL
 #define F3_SUNROLL 4   // hit-loop unroll
 #endif
@@ -221,7 +256,12 @@ template <bool ARC, int MODE, int RPL, bool PFX, int NW>
 __global__ void __launch_bounds__(32 * NW, F3_MINB * F3_NWARPS / NW)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
-       const float* __restrict__ w, float* __restrict__ out, int pfx_stride) {
+       const float* __restrict__ w, float* __restrict__ out, int pfx_stride, int slot_entries) {
+    constexpr bool TMA = PFX && F3_TMA;
+    constexpr int TD = F3_TMAD;
+    extern __shared__ __align__(16) float2 fwd_ring[];   // TMA: [NW][TD][slot_entries]
+    __shared__ __align__(8) unsigned long long fbar[TMA ? NW : 1][TMA ? TD : 1];
+    __shared__ int2 qR[TMA ? NW : 1][32];   // TMA: (global element offset of the run, first entry | entries << 16)
     __shared__ float4 qL[NW][32];    // L for the 4 detector columns
     __shared__ float4 qG[NW][32];    // PFX: (1/(H nz), -B0/(H nz), column offset, X(top)); direct: (B0, H, col, -)
     __shared__ float stage[32 * RPL][(NW * F3_CPW) + 1];
@@ -244,6 +284,14 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     const float cb = vw.x, sb = vw.y, zs = vw.z;
     const float Sx = G.dso * cb, Sy = G.dso * sb;
     const unsigned lanemask_lt = (1u << lane) - 1u;
+    unsigned tcnt = 0;   // TMA: bulk copies consumed by this warp (ring slot and phase)
+    if (TMA) {
+        if (lane == 0) {
+            for (int q = 0; q < TD; q++) mbar_init(smem_u32(&fbar[wid][q]));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
 
     float acc[F3_CPW][RPL];
 #pragma unroll
@@ -333,6 +381,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 const int o = lo + sub + F3_SUB * p;
                 bool nz = false;
                 float4 eL = make_float4(0.f, 0.f, 0.f, 0.f), eG = make_float4(0.f, 0.f, 0.f, 0.f);
+                int2 eR = make_int2(0, 0);
                 if (o <= hi) {
                     const int i = xstep ? sl : o, j = xstep ? o : sl;
                     const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
@@ -366,6 +415,15 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         CTR_CHECK((unsigned long long)(cbq + __float_as_uint(rt)) <
                                       (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd top gather");
                         qt = __ldg(Q + (cbq + __float_as_uint(rt)));
+                        if (TMA) {
+                            // entries the lanes' rows reach: k(row 0) .. k(row RPL 32), monotone in the row
+                            const float f0 = fmaf(__saturatef(bg), fnz, -0.5f);
+                            const int kb = __float_as_int(__fadd_rn(f0, 12582912.0f)) - 0x4B400000;
+                            const int kt = __float_as_int(rt) - 0x4B400000;
+                            const int klo = kb & ~1, cnt = (kt + 2 - klo) & ~1;   // 16-byte aligned run
+                            CTR_CHECK(cnt <= slot_entries && klo >= 0 && klo + cnt <= pfx_stride, "fwd run");
+                            eR = make_int2((int)(cbq + 0x4B400000u) + klo, klo | (cnt << 16));
+                        }
                     }
                     if (cand) {
                         fp_trans<ARC>(G, cb, sb, fb, f);
@@ -397,8 +455,17 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     CTR_CHECK(slot < 32, "fwd queue slot");
                     qL[wid][slot] = eL;
                     qG[wid][slot] = eG;
+                    if (TMA) qR[wid][slot] = eR;
                 }
                 __syncwarp();
+                if (TMA && lane == 0) {
+                    for (int q = 0; q < min(TD, n); q++) {
+                        const unsigned sl = (tcnt + q) % TD;
+                        const int2 R = qR[wid][q];
+                        bulk_copy(smem_u32(fwd_ring + (wid * TD + sl) * slot_entries), Q + (unsigned)R.x,
+                                  (unsigned)(R.y >> 16) * 8u, smem_u32(&fbar[wid][sl]));
+                    }
+                }
 #pragma unroll (kF3SingleUnroll)
                 for (int e = 0; e < n; e++) {
                     const float4 L4 = qL[wid][e];
@@ -416,15 +483,40 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         // Unsigned 32-bit element offsets.
                         const unsigned cq = __float_as_uint(q.z);
                         float Xp[RPL];
+                        const float2* __restrict__ run = nullptr;
+                        int klo = 0;
+                        unsigned sl = 0;
+                        if (TMA) {
+                            sl = (tcnt + e) % TD;
+                            mbar_wait(smem_u32(&fbar[wid][sl]), ((tcnt + e) / TD) & 1);
+                            klo = qR[wid][e].y & 0xffff;
+                            run = fwd_ring + (wid * TD + sl) * slot_entries - klo;
+                        }
 #pragma unroll
                         for (int r = 0; r < RPL; r++) {
                             const float g = __saturatef(fmaf((float)fwd_row<RPL>(lane, r), q.x, q.y));
                             const float f = fmaf(g, fnz, -0.5f);
                             const float rm = __fadd_rn(f, 12582912.0f);
-                            CTR_CHECK((unsigned long long)(cq + __float_as_uint(rm)) <
-                                          (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd prefix gather");
-                            const float2 qk = __ldg(Q + (cq + __float_as_uint(rm)));
+                            float2 qk;
+                            if (TMA) {
+                                const int k = __float_as_int(rm) - 0x4B400000;
+                                CTR_CHECK(k >= klo && k < klo + (qR[wid][e].y >> 16), "fwd run entry");
+                                qk = run[k];
+                            } else {
+                                CTR_CHECK((unsigned long long)(cq + __float_as_uint(rm)) <
+                                              (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd prefix gather");
+                                qk = __ldg(Q + (cq + __float_as_uint(rm)));
+                            }
                             Xp[r] = fmaf(f, qk.y, qk.x);
+                        }
+                        if (TMA) {
+                            // every lane has read slot sl: refill it with hit e + TD
+                            __syncwarp();
+                            if (lane == 0 && e + TD < n) {
+                                const int2 R = qR[wid][e + TD];
+                                bulk_copy(smem_u32(fwd_ring + (wid * TD + sl) * slot_entries), Q + (unsigned)R.x,
+                                          (unsigned)(R.y >> 16) * 8u, smem_u32(&fbar[wid][sl]));
+                            }
                         }
                         if (F3_STRIDED) {
                             float v[RPL];
@@ -472,6 +564,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         acc[3][r] = fmaf(L4.w, Rs[r], acc[3][r]);
                     }
                 }
+                if (TMA) tcnt += n;
                 __syncwarp();
             }
         }
@@ -512,13 +605,32 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 }
 
+// TMA variant: entries of the longest run a hit can need — RPL 32 detector rows over the smallest
+// voxel height H_min = dz Dsd / ((Dso + r_xy) dt) (the magnification of the farthest voxel) — plus
+// rounding and alignment, at most a whole column
+static int fwd_slot_entries(const DGeom& G, int rpl, int ps) {
+    const double hmin = (double)G.dz * G.dsd / ((double)G.dso + G.rxy) * G.inv_dt;
+    const int run = (int)std::ceil(32.0 * rpl / hmin) + 6;
+    return std::min(ps, (run + 1) & ~1);
+}
+
+template <bool ARC, int MODE, int RPL, bool PFX, int NW>
+static void fwd3_launch(const DGeom& G, dim3 grid, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
+                        const float* xb, const float* y, const float* w, float* out, int ps, cudaStream_t s) {
+    const int se = (PFX && F3_TMA) ? fwd_slot_entries(G, RPL, ps) : 0;
+    const size_t smem = (size_t)NW * F3_TMAD * se * sizeof(float2);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_fwd3<ARC, MODE, RPL, PFX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_fwd3<ARC, MODE, RPL, PFX, NW><<<grid, 32 * NW, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps, se);
+}
+
 template <bool ARC, int MODE, bool PFX, int NW>
 static void fwd3_nw(const DGeom& G, int max_count, const float4* vtab, const Ctl* ctl, Views v, const float* xa,
                     const float* xb, const float* y, const float* w, float* out, int ps, cudaStream_t s) {
     dim3 grid((G.ns + NW * F3_CPW - 1) / (NW * F3_CPW), max_count);
-    if (G.nt <= 32) k_fwd3<ARC, MODE, 1, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
-    else if (G.nt <= 64) k_fwd3<ARC, MODE, 2, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
-    else k_fwd3<ARC, MODE, 4, PFX, NW><<<grid, 32 * NW, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps);
+    if (G.nt <= 32) fwd3_launch<ARC, MODE, 1, PFX, NW>(G, grid, vtab, ctl, v, xa, xb, y, w, out, ps, s);
+    else if (G.nt <= 64) fwd3_launch<ARC, MODE, 2, PFX, NW>(G, grid, vtab, ctl, v, xa, xb, y, w, out, ps, s);
+    else fwd3_launch<ARC, MODE, 4, PFX, NW>(G, grid, vtab, ctl, v, xa, xb, y, w, out, ps, s);
 }
 
 // 2-warp blocks when 4-warp blocks would fill fewer than two waves (8 blocks per SM)
