@@ -18,8 +18,13 @@ from synth.configs import get_config  # noqa: E402
 
 
 def main():
-    name = sys.argv[1] if len(sys.argv) > 1 else "c4"
-    worlds = [int(a) for a in sys.argv[2:]] or [1, 2, 4, 8]
+    args = sys.argv[1:]
+    if "--lib" in args:   # a tuning variant of the library (scripts/build_variants.py)
+        i = args.index("--lib")
+        C.LIB_PATH = os.path.abspath(args[i + 1])
+        del args[i:i + 2]
+    name = args[0] if len(args) > 0 else "c4"
+    worlds = [int(a) for a in args[1:]] or [1, 2, 4, 8]
     cfg = get_config(name)
     inp = bench.make_inputs(cfg, "cuda")
     g = cfg["geom"]

@@ -53,7 +53,9 @@ def mid(kind, **over):
       helical_rpl4  flat, nt = 96 (four rows per lane), 4-warp forward over all views, nz = 80
                     (four 24-voxel z-chunks, the last ragged: the back-projector's chunks share
                     each column's footprint)
-      axial_mid     flat axial, nt = 40, nz = 50 (two update z-chunks)"""
+      axial_mid     flat axial, nt = 40, nz = 50 (two update z-chunks)
+      helical_thin  helical_mid with 12 planes: every hit spans <= 32 detector rows (one row
+                    per lane in the z-prefix forward, as in thin z-slabs)"""
     if kind == "helical_mid":
         g = _geom(dim=3, nx=36, ny=36, nz=56, dx=1.0, dy=1.0, dz=1.0, det="arc", ns=160, nt=64,
                   ds=0.625, dt=1.0, offset_s=0.75, offset_t=-0.3, dso=100.0, dsd=180.0, na=480,
@@ -64,6 +66,10 @@ def mid(kind, **over):
                   ds=0.7, dt=0.8, offset_s=-0.6, offset_t=0.4, dso=100.0, dsd=180.0, na=300,
                   orbit_deg=720.0, pitch=0.9, orbit_start_deg=5.0)
         g["source_z0"] = _helical_z0(g["na"], g["nt"], g["dt"], g["dso"], g["dsd"], 0.9, 720.0)
+    elif kind == "helical_thin":
+        # helical_mid cut to 12 planes: a voxel column spans 17-29 detector rows, so the z-prefix
+        # forward takes one row per lane (the path of thin z-slabs)
+        g = mid("helical_mid", nz=12, dz=1.0)
     elif kind == "axial_mid":
         g = _geom(dim=3, nx=40, ny=40, nz=50, dx=1.0, dy=1.0, dz=1.0, det="flat", ns=120, nt=40,
                   ds=0.95, dt=1.6, offset_s=0.25, offset_t=0.1, dso=110.0, dsd=200.0, na=240)
@@ -73,7 +79,7 @@ def mid(kind, **over):
     return copy.deepcopy(g)
 
 
-MID_KINDS = ["helical_mid", "helical_rpl4", "axial_mid"]
+MID_KINDS = ["helical_mid", "helical_rpl4", "axial_mid", "helical_thin"]
 
 
 def fwd3_blocks(g, count):

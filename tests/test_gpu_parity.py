@@ -621,14 +621,15 @@ def test_nccl_sharded_path_world1_matches_single_gpu(C, kind):
 
 
 @pytest.mark.parametrize("kind,world", [("helical_arc", 2), ("helical_arc", 3), ("axial_flat", 2),
-                                        ("helical_fine", 3), ("fan2d_arc", 1)])
+                                        ("helical_fine", 3), ("fan2d_arc", 1), ("helical_mid", 4)])
 def test_zslab_decomposition_matches_single_gpu(C, kind, world):
     """the z-slab decomposition with `world` slabs driven by one
     process (partial projections summed on the device, halos copied) matches the
     float64 oracle (Algorithm 1 trace: D_L, and x, g, htilde after 7 sub-iterations
     split over two calls) and equals the fused single-GPU solve."""
     from paper_1512_04564_b200.recon import Recon
-    pb = synthetic_problem(tiny(kind), M=3)
+    from tests.geoms import mid
+    pb = synthetic_problem(mid(kind) if kind.endswith("_mid") else tiny(kind), M=3)
     trace = {}
     alg.alg1(oracle_problem(pb), pb["x0"], 3, 1.999, 3, DL=pb["DL"], trace=trace)
     xo, go, ho = trace[7]
