@@ -235,9 +235,6 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
 #ifndef F3_SUNROLL
 #define F3_SUNROLL 4   // hit-loop unroll
 #endif
-#ifndef F3_NARROW
-#define F3_NARROW 1    // PFX, >= 2 rows per lane: hits spanning <= 32 detector rows use one row per lane
-#endif
 #ifndef F3_STRIDED
 #define F3_STRIDED 0   // lane l owns detector rows RPL l + r (0) or l + 32 r (1)
 #endif
@@ -267,12 +264,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     __shared__ int2 qR[TMA ? NW : 1][32];   // TMA: (global element offset of the run, first entry | entries << 16)
     __shared__ float4 qL[NW][32];    // L for the 4 detector columns
     __shared__ float4 qG[NW][32];    // PFX: (1/(H nz), -B0/(H nz), column offset, X(top)); direct: (B0, H, col, -)
-    // NARROW: hits whose column spans at most 32 detector rows (thin z-slabs) take one row per lane
-    // and accumulate into their warp's columns of the stage (float4 rows: 16-byte aligned)
-    constexpr bool NARROW = PFX && F3_NARROW && RPL >= 2;
-    constexpr int SROW = NARROW ? (NW * F3_CPW) + 4 : (NW * F3_CPW) + 1;
-    __shared__ __align__(16) float stage[32 * RPL][SROW];
-    __shared__ int qT[NARROW ? NW : 1][32];   // NARROW: first detector row of the hit, or -1
+    __shared__ float stage[32 * RPL][(NW * F3_CPW) + 1];
 #if F3_PREYW
     __shared__ float ysm[MODE == FWD_RESID ? 32 * RPL : 1][(NW * F3_CPW)];   // epilogue operands (cp.async)
     __shared__ float wsm[MODE != FWD_PLAIN ? 32 * RPL : 1][(NW * F3_CPW)];
@@ -306,12 +298,6 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
         for (int r = 0; r < RPL; r++) acc[c][r] = 0.f;
-    if (NARROW) {   // the warp's own stage columns (warp-private until the epilogue's barrier)
-#pragma unroll
-        for (int r = 0; r < RPL; r++)
-            *reinterpret_cast<float4*>(&stage[lane + 32 * r][wid * F3_CPW]) = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncwarp();
-    }
 
 #if F3_PREYW
     // y and w of the block's (row, column) outputs are read only by the epilogue: start their
@@ -396,7 +382,6 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 bool nz = false;
                 float4 eL = make_float4(0.f, 0.f, 0.f, 0.f), eG = make_float4(0.f, 0.f, 0.f, 0.f);
                 int2 eR = make_int2(0, 0);
-                int tn = -1;   // NARROW: the hit's first detector row
                 if (o <= hi) {
                     const int i = xstep ? sl : o, j = xstep ? o : sl;
                     const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
@@ -424,13 +409,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         ih = invH * rnz;
                         bg = fmaf(-f.B0, invH, 0.f) * rnz;
                         cbq = (unsigned)(j * G.nx + i) * (unsigned)pfx_stride - 0x4B400000u;
-                        if (NARROW) {
-                            // rows [t0, t0 + 32) cover the column (one row of margin above its top)
-                            const int t0 = max((int)floorf(f.B0), 0);
-                            const int t1 = (int)ceilf(fmaf(fnz, f.H, f.B0)) + 1;
-                            if (min(t1, G.nt) - t0 <= 32 && t0 + 32 <= 32 * RPL) tn = t0;
-                        }
-                        const float gt = __saturatef(fmaf((float)(tn >= 0 ? tn + 32 : RPL * 32), ih, bg));
+                        const float gt = __saturatef(fmaf((float)(RPL * 32), ih, bg));
                         ft = fmaf(gt, fnz, -0.5f);
                         const float rt = __fadd_rn(ft, 12582912.0f);
                         CTR_CHECK((unsigned long long)(cbq + __float_as_uint(rt)) <
@@ -477,7 +456,6 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     qL[wid][slot] = eL;
                     qG[wid][slot] = eG;
                     if (TMA) qR[wid][slot] = eR;
-                    if (NARROW) qT[wid][slot] = tn;
                 }
                 __syncwarp();
                 if (TMA && lane == 0) {
@@ -493,31 +471,6 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     const float4 L4 = qL[wid][e];
                     const float4 q = qG[wid][e];
                     const int col = __float_as_int(q.z);
-                    if (NARROW) {
-                        const int tl = qT[wid][e];
-                        if (tl >= 0) {   // warp-uniform: one row per lane, rows tl .. tl + 31
-                            const float g = __saturatef(fmaf((float)(tl + lane), q.x, q.y));
-                            const float f = fmaf(g, fnz, -0.5f);
-                            const float rm = __fadd_rn(f, 12582912.0f);
-                            const unsigned cq = __float_as_uint(q.z);
-                            CTR_CHECK((unsigned long long)(cq + __float_as_uint(rm)) <
-                                          (unsigned long long)G.nxy * (unsigned)pfx_stride, "fwd narrow gather");
-                            const float2 qk = __ldg(Q + (cq + __float_as_uint(rm)));
-                            const float X = fmaf(f, qk.y, qk.x);
-                            const float xn = __shfl_down_sync(0xffffffffu, X, 1);
-                            const float rs = (lane == 31 ? q.w : xn) - X;
-                            CTR_CHECK(tl + lane < 32 * RPL, "fwd narrow row");
-                            float4* __restrict__ sp = reinterpret_cast<float4*>(&stage[tl + lane][wid * F3_CPW]);
-                            float4 a = *sp;
-                            a.x = fmaf(L4.x, rs, a.x);
-                            a.y = fmaf(L4.y, rs, a.y);
-                            a.z = fmaf(L4.z, rs, a.z);
-                            a.w = fmaf(L4.w, rs, a.w);
-                            *sp = a;
-                            __syncwarp();   // the next narrow hit's lanes read these rows
-                            continue;
-                        }
-                    }
                     float Rs[RPL];   // F2-weighted row sums of this voxel column
                     if (PFX) {
                         // X(u) = A_k + f x_k (A_k = P_k - (k - 1/2) x_k; f the voxel coordinate
@@ -621,10 +574,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #pragma unroll
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
-        for (int r = 0; r < RPL; r++) {
-            float& st = stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c];
-            st = NARROW ? st + acc[c][r] : acc[c][r];
-        }
+        for (int r = 0; r < RPL; r++) stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c] = acc[c][r];
 #if F3_PREYW
     if (YW) asm volatile("cp.async.wait_all;" ::: "memory");
 #endif
