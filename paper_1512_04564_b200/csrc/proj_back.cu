@@ -96,6 +96,7 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
 #ifndef BK_WMAX
 #define BK_WMAX 6      // widest register window of detector columns (wider footprints: general loop)
 #endif
+
 template <bool ARC, bool LZ, int W>
 __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WMAX], const float* __restrict__ pr,
                                           int sw, int tw, int n, float2* __restrict__ cs, float& run) {

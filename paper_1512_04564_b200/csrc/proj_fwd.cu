@@ -232,8 +232,17 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
                  : "memory");
 }
 
+#ifndef F3_WCSMEM
+#define F3_WCSMEM 1    // the candidate walk's per-warp constants in shared memory (frees registers)
+#endif
+struct WalkC {
+    float nlx, nly, nrx, nry, suppl, suppr, tol_l, tol_r, kl, kr, Sa, So, a0, da, ha, o0, inv_do, sgn, Sx, Sy, cb, sb,
+        zs;
+    int na_, no_;
+    bool xstep;
+};
 #ifndef F3_SUNROLL
-#define F3_SUNROLL 4   // hit-loop unroll
+#define F3_SUNROLL 8   // hit-loop unroll (8: c4 fwd 2.51 -> 2.31 ms with F3_WCSMEM, r2o)
 #endif
 #ifndef F3_STRIDED
 #define F3_STRIDED 0   // lane l owns detector rows RPL l + r (0) or l + 32 r (1)
@@ -262,6 +271,9 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     extern __shared__ __align__(16) float2 fwd_ring[];   // TMA: [NW][TD][slot_entries]
     __shared__ __align__(8) unsigned long long fbar[TMA ? NW : 1][TMA ? TD : 1];
     __shared__ int2 qR[TMA ? NW : 1][32];   // TMA: (global element offset of the run, first entry | entries << 16)
+#if F3_WCSMEM
+    __shared__ WalkC wcs[NW];
+#endif
     __shared__ float4 qL[NW][32];    // L for the 4 detector columns
     __shared__ float4 qG[NW][32];    // PFX: (1/(H nz), -B0/(H nz), column offset, X(top)); direct: (B0, H, col, -)
     __shared__ float stage[32 * RPL][(NW * F3_CPW) + 1];
@@ -358,21 +370,38 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
         const float inv_do = 1.f / dob;
         const float fnz = (float)G.nz, rnz = 1.f / (float)G.nz;
+#if F3_WCSMEM
+        // the walk's per-warp constants live in shared memory (volatile reads in the producer) so that
+        // they do not hold registers through the hit loop
+        if (lane == 0) {
+            volatile WalkC* wv = &wcs[wid];
+            wv->nlx = nlx; wv->nly = nly; wv->nrx = nrx; wv->nry = nry; wv->suppl = suppl; wv->suppr = suppr;
+            wv->tol_l = tol_l; wv->tol_r = tol_r; wv->kl = kl; wv->kr = kr; wv->Sa = Sa; wv->So = So;
+            wv->a0 = a0; wv->da = da; wv->ha = ha; wv->o0 = o0; wv->inv_do = inv_do; wv->sgn = sgn;
+            wv->Sx = Sx; wv->Sy = Sy; wv->na_ = na_; wv->no_ = no_; wv->xstep = xstep; wv->cb = cb; wv->sb = sb;
+            wv->zs = zs;
+        }
+        __syncwarp();
+        const volatile WalkC* wcv = &wcs[wid];
+#define WCX(v) (wcv->v)
+#else
+#define WCX(v) (v)
+#endif
 
-        for (int sl0 = 0; sl0 < na_; sl0 += 32 / F3_SUB) {
+        for (int sl0 = 0; sl0 < WCX(na_); sl0 += 32 / F3_SUB) {
             const int sl = sl0 + lane / F3_SUB, sub = lane % F3_SUB;
             int lo = 0, hi = -1;
-            if (sl < na_) {
-                const float ac = fmaf((float)sl, da, a0);
-                const float pa = ac - ha - Sa, pb = ac + ha - Sa;
-                if (pa * sgn > 0.f && pb * sgn > 0.f) {
-                    const float y1 = fmaf(pa, kl, So), y2 = fmaf(pb, kl, So);
-                    const float y3 = fmaf(pa, kr, So), y4 = fmaf(pb, kr, So);
-                    const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - o0) * inv_do + 0.5f;
-                    const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - o0) * inv_do + 0.5f;
-                    if (f1 >= -1.f && f0 <= (float)no_ + 1.f) {
+            if (sl < WCX(na_)) {
+                const float ac = fmaf((float)sl, WCX(da), WCX(a0));
+                const float pa = ac - WCX(ha) - WCX(Sa), pb = ac + WCX(ha) - WCX(Sa);
+                if (pa * WCX(sgn) > 0.f && pb * WCX(sgn) > 0.f) {
+                    const float y1 = fmaf(pa, WCX(kl), WCX(So)), y2 = fmaf(pb, WCX(kl), WCX(So));
+                    const float y3 = fmaf(pa, WCX(kr), WCX(So)), y4 = fmaf(pb, WCX(kr), WCX(So));
+                    const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - WCX(o0)) * WCX(inv_do) + 0.5f;
+                    const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - WCX(o0)) * WCX(inv_do) + 0.5f;
+                    if (f1 >= -1.f && f0 <= (float)WCX(no_) + 1.f) {
                         lo = max((int)floorf(f0 - 1e-3f), 0);
-                        hi = min((int)floorf(f1 + 1e-3f), no_ - 1);
+                        hi = min((int)floorf(f1 + 1e-3f), WCX(no_) - 1);
                     }
                 }
             }
@@ -383,17 +412,17 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                 float4 eL = make_float4(0.f, 0.f, 0.f, 0.f), eG = make_float4(0.f, 0.f, 0.f, 0.f);
                 int2 eR = make_int2(0, 0);
                 if (o <= hi) {
-                    const int i = xstep ? sl : o, j = xstep ? o : sl;
-                    const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
-                    const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
+                    const int i = WCX(xstep) ? sl : o, j = WCX(xstep) ? o : sl;
+                    const float cx = fmaf((float)i, G.dx, G.x0) - WCX(Sx);
+                    const float cy = fmaf((float)j, G.dy, G.y0) - WCX(Sy);
                     FpBase fb;
                     Footprint f;
-                    bool cand = fmaf(nlx, cx, nly * cy) + suppl >= -tol_l && fmaf(nrx, cx, nry * cy) + suppr >= -tol_r;
+                    bool cand = fmaf(WCX(nlx), cx, WCX(nly) * cy) + WCX(suppl) >= -WCX(tol_l) && fmaf(WCX(nrx), cx, WCX(nry) * cy) + WCX(suppr) >= -WCX(tol_r);
                     if (cand) {
                         // axial extent first: a column whose magnified extent misses the detector
                         // rows (helical views near the ends of the helix) is not queued
-                        fp_base(G, cb, sb, i, j, fb);
-                        fp_axial<ARC>(G, fb, zs, f.B0, f.H);
+                        fp_base(G, WCX(cb), WCX(sb), i, j, fb);
+                        fp_axial<ARC>(G, fb, WCX(zs), f.B0, f.H);
                         cand = f.B0 < (float)G.nt && fmaf(fnz, f.H, f.B0) > 0.f;
                     }
                     // PFX: the top-boundary gather (lane 31's upper row edge) is issued before the
@@ -426,7 +455,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         }
                     }
                     if (cand) {
-                        fp_trans<ARC>(G, cb, sb, fb, f);
+                        fp_trans<ARC>(G, WCX(cb), WCX(sb), fb, f);
                         // F1 of the 4 detector columns from 5 edge evaluations
                         float T0 = trap_T(f, ((float)s0 - 0.5f) - f.sfc);
                         float Fc[F3_CPW];
@@ -570,6 +599,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         }
     }
 
+#undef WCX
     // epilogue: stage [row][detector column in block], then each thread handles one (row, column)
 #pragma unroll
     for (int c = 0; c < F3_CPW; c++)

@@ -664,8 +664,10 @@ def test_zslab_decomposition_matches_single_gpu(C, kind, world):
         assert rel(xg, xo) <= 1e-4, rel(xg, xo)
         assert rel(gg_, go) <= 1e-3
         assert rel(hg, pb["DL"] * xo - ho) <= 1e-3
-        for got, exp in zip((xg, gg_, hg), want):
-            assert rel(got, exp) <= 1e-5, rel(got, exp)
+        # against the fused single-GPU solve: the slabs' partial projections are summed in another
+        # order (and each slab's z-prefix restarts at its bottom plane), float32 rounding only
+        for name, got, exp in zip(("x", "g", "htilde"), (xg, gg_, hg), want):
+            assert rel(got, exp) <= 5e-5, (name, rel(got, exp))
     finally:
         C.ct_geom_destroy(h)
 
