@@ -382,6 +382,9 @@ static UpdShape upd_shape(const DGeom& G, bool pfx) {
     UpdShape u;
     constexpr int zdiv = UPD_ZDIV;   // voxels per z-chunk target (tuning variants: -DUPD_ZDIV=n)
     u.nzc = std::min(8, std::max(1, G.nz / std::max(1, zdiv)));
+    // at least 4 chunks once a column has 64 planes (c3: 4 x 16 instead of 2 x 32 planes, 0.086 ->
+    // 0.077 ms, r2q; c4 keeps 4 x 24, c5 8 x 32)
+    if (G.nz >= 64) u.nzc = std::max(u.nzc, 4);
     u.cz = (G.nz + u.nzc - 1) / u.nzc;
     u.nzc = (G.nz + u.cz - 1) / u.cz;
     u.jpb = std::max(1, 8 / u.nzc);  // JPB rows per block share x rows in L1
