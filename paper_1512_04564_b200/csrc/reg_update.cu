@@ -54,10 +54,15 @@ __device__ __forceinline__ float omega_scaled(float tp, const RegParams& rp) {
 // kappa_n); grad = delta gs, curv = 2 cs.  CHECK = false is the interior path:
 // every neighbour exists, no predicates, and without kappa the two
 // neighbours of a direction share one beta multiply.
-template <int NDIRS, bool KAPPA, int POT, int ZA, int ZB, int ZC, bool CHECK>
+// PATH: 0 interior (every neighbour exists), 1 checked (any border), 2 x-border only (every y and z
+// neighbour exists): the interior arithmetic with the differences to the missing x neighbours
+// selected to 0 (their gradient term vanishes) and their curvature terms, beta_d omega(0) = beta_d
+// each, subtracted afterwards (xcorr = (!im + !ip) sum_{d: ox != 0} beta_d, per column).
+template <int NDIRS, bool KAPPA, int POT, int ZA, int ZB, int ZC, int PATH>
 __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const float (&K)[4][3][3],
                                                const RegParams& rp, bool im, bool ip, bool jm, bool jp, bool km,
-                                               bool kp, float& gs_out, float& cs_out) {
+                                               bool kp, float xcorr, float& gs_out, float& cs_out) {
+    constexpr bool CHECK = PATH == 1;
     const float xv = W[ZB][1][1];
     const float kj = KAPPA ? K[ZB][1][1] : 1.f;
     float gs = 0.f, cs = 0.f, cmax = 0.f;
@@ -69,7 +74,11 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
         const int ox = dir_x(d), oy = dir_y(d), oz = dir_z(d);
         const int zp = oz > 0 ? ZC : ZB, zm = oz > 0 ? ZA : ZB;
         if (!CHECK && !KAPPA) {
-            const float2 t = make_float2(xv - W[zp][1 + oy][1 + ox], xv - W[zm][1 - oy][1 - ox]);
+            float2 t = make_float2(xv - W[zp][1 + oy][1 + ox], xv - W[zm][1 - oy][1 - ox]);
+            if (PATH == 2 && ox != 0) {
+                t.x = (ox > 0 ? ip : im) ? t.x : 0.f;
+                t.y = (ox > 0 ? im : ip) ? t.y : 0.f;
+            }
             float2 o;
             if (POT == 1) {
                 const float2 u = fma2(t, t, bcast2(1.f));
@@ -101,10 +110,11 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
     if (!CHECK && !KAPPA) {
         gs = gs2.x + gs2.y;
         cs = cs2.x + cs2.y;
+        if (PATH == 2) cs -= xcorr;
     }
     gs_out = gs;
     // maximum curvature: omega(0) = 1 for every in-volume neighbour (interior, no kappa: bsum)
-    cs_out = rp.maxcurv ? ((!CHECK && !KAPPA) ? rp.bsum : cmax) : cs;
+    cs_out = rp.maxcurv ? ((!CHECK && !KAPPA) ? (PATH == 2 ? rp.bsum - xcorr : rp.bsum) : cmax) : cs;
 }
 
 // Arguments of the update-family kernels (k_update, k_update_pre).
@@ -198,6 +208,12 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     const bool im = i > 0, ip = i + 1 < G.nx, jm = j > 0, jp = j + 1 < G.ny;
     const bool inxy = act && im && ip && jm && jp;
     const bool wfast = __all_sync(0xffffffffu, !act || inxy);   // warp-uniform stencil path (no divergence)
+    const bool wxedge = !KAPPA && __all_sync(0xffffffffu, !act || (jm && jp));   // x-border only: PATH 2
+    float xcorr = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIRS; d++)
+        if (dir_x(d) != 0) xcorr += rp.beta[d];
+    xcorr *= (float)(!im) + (float)(!ip);
     const unsigned nx = (unsigned)G.nx, nxy = (unsigned)G.nxy;
     const unsigned col = act ? (unsigned)j * nx + (unsigned)i : 0u;
     const int k0 = c * A.CZ, k1 = min(G.nz, k0 + A.CZ);
@@ -278,11 +294,14 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         if (act) {
             const unsigned idx = (unsigned)k * nxy + col;
             float gs, cs;
-            const bool km = k > 0 || A.halo_lo, kp = k + 1 < G.nz || A.halo_hi;
+            // (2-D: no z neighbours, so the z borders do not force the checked stencil)
+            const bool km = NDIRS == 4 || k > 0 || A.halo_lo, kp = NDIRS == 4 || k + 1 < G.nz || A.halo_hi;
             if (wfast && km && kp)
-                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, false>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 0>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
+            else if (wxedge && km && kp)
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 2>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
             else
-                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, true>(W, K, rp, im, ip, jm, jp, km, kp, gs, cs);
+                window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 1>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
             if (FULL) {
                 const float xv = XC[ZB];
                 const float d = Dv[Q], htv = Hv[Q];
