@@ -504,8 +504,7 @@ static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, flo
     launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, xt, s);
     if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, r, FWD_RESID, s, pfx_stride_of(g->G));
     else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
-    launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);
-    launch_advance(ctl, s);
+    launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);   // + k advance
 }
 
 static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, const ct_reg_desc* r,
@@ -638,7 +637,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             e = cudaGraphInstantiate(&exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) return fail(CT_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-            launches_add(-4);  // capture is not a launch; replays are counted below
+            launches_add(-3);  // capture is not a launch; replays are counted below
             const_cast<ct_geom*>(g)->graphs[key] = exec;
         }
     }
@@ -699,7 +698,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         cudaEvent_t* ev = kernel_ms ? &evs[(size_t)done * 5] : nullptr;
         if (exec) {
             CT_CUDA(cudaGraphLaunch(exec, s));
-            launches_add(4);
+            launches_add(3);
         } else if (!dist) {
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
@@ -709,8 +708,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
             launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g, st->htilde, s);
-            if (ev) CT_CUDA(cudaEventRecord(ev[3], s));
-            launch_advance(ctl, s);
+            if (ev) CT_CUDA(cudaEventRecord(ev[3], s));   // (the back-projection's last block advanced k)
             if (ev) CT_CUDA(cudaEventRecord(ev[4], s));
         } else {
             // Multi-GPU sub-iteration: this rank's views are projected, the partial

@@ -67,7 +67,26 @@ struct Ctl {
     int simple;         // Algorithm 2: the htilde array holds zeta
     float alpha, rho_fixed;
     int bad;            // set by kernels on footprint overflow (debug guard)
+    unsigned done;      // blocks of the current back-projection finished (advance_after_last_block)
 };
+
+// Algorithm 1 line 9 (k <- k + 1) folded into the back-projection that ends a
+// sub-iteration: the last block to finish advances the counter and resets the block count
+// (no separate one-thread launch).  Every thread of every block must reach this call; the
+// other blocks' reads of k (view selection, rho) are complete by then.
+__device__ __forceinline__ void advance_after_last_block(const Ctl* ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+        Ctl* c = const_cast<Ctl*>(ctl);
+        __threadfence();
+        const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+        if (atomicAdd(&c->done, 1u) == nb - 1) {
+            c->done = 0;
+            c->k += 1;
+            __threadfence();
+        }
+    }
+}
 
 struct Views {          // explicit descriptor, or subset-from-Ctl when ctl != nullptr
     int start, stride, count;

@@ -63,28 +63,29 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     if (VS > 1) {
         red[part][threadIdx.y][threadIdx.x] = acc;
         __syncthreads();
-        if (part != 0) return;
         acc = 0.f;
 #pragma unroll
         for (int q = 0; q < VS; q++) acc += red[q][threadIdx.y][threadIdx.x];
     }
-    if (!act) return;
-    const size_t idx = (size_t)j * G.nx + i;
-    const float z = scale * acc;
-    if (EPI == BK_WRITE) {
-        out[idx] = z;
+    // (no early returns: with BK_UPDATE every thread reaches advance_after_last_block)
+    if (!act || part != 0) {
+    } else if (EPI == BK_WRITE) {
+        out[(size_t)j * G.nx + i] = scale * acc;
     } else if (EPI == BK_ACCUM) {
-        out[idx] += z;
+        out[(size_t)j * G.nx + i] += scale * acc;
     } else if (EPI == BK_INIT) {
-        gbuf[idx] = z;
-        htbuf[idx] = z;
+        gbuf[(size_t)j * G.nx + i] = scale * acc;
+        htbuf[(size_t)j * G.nx + i] = scale * acc;
     } else {
+        const size_t idx = (size_t)j * G.nx + i;
+        const float z = scale * acc;
         const float rho = rho_of_k(ctl), alpha = ctl->alpha;
         const float gv = gbuf[idx];
         const float inv = 1.f / (rho + 1.f);
         gbuf[idx] = fmaf(rho * inv, fmaf(alpha, z, (1.f - alpha) * gv), gv * inv);
         htbuf[idx] = ctl->simple ? z : fmaf(alpha, z, htbuf[idx]);
     }
+    if (EPI == BK_UPDATE) advance_after_last_block(ctl);
 }
 
 // Row sums of one (voxel column, view) over a window of W detector columns:
@@ -191,7 +192,11 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     const int nstage = max(0, min(vi1 - vi0, BK_VSM));
     for (int q = tid; q < nstage; q += BK_BS) vsm[q] = __ldg(&vtab[V.start + (vi0 + q) * V.stride]);
     __syncthreads();
-    if (i >= G.nx || j >= G.ny) return;
+    const bool act3 = i < G.nx && j < G.ny;
+    if (!act3) {
+        if (EPI != BK_UPDATE) return;
+        vi1 = vi0;   // BK_UPDATE: no views, no epilogue, but the block's completion is counted
+    }
     float2* __restrict__ cs = &csb[0][tid];
 
     float acc[BK_KZ];
@@ -306,7 +311,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
     }
 
     // epilogue
-    const int kz = min(BK_KZ, G.nz - k0);
+    const int kz = act3 ? min(BK_KZ, G.nz - k0) : 0;
     if (EPI == BK_UPDATE) {
         // lines 7-8: g and htilde of the chunk in batches of EB voxels, every load of a batch
         // issued before its first use (one HBM round trip per batch instead of per voxel)
@@ -337,6 +342,7 @@ k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
                 }
             }
         }
+        advance_after_last_block(ctl);
     } else {
 #pragma unroll
         for (int q = 0; q < BK_KZ; q++) {

@@ -383,8 +383,7 @@ extern "C" ct_status oslalm_zslab_solve(const ct_geom* g, const float* y, const 
         if (st != CT_OK) return st;
         for (int i = 0; i < nlocal; i++) {
             launch_back(sl[i].S, vtab, sl[i].ctl, Views{0, 1, 0}, rbuf, (float)M, BK_UPDATE, false, nullptr, st_[i].g,
-                        st_[i].htilde, s);
-            launch_advance(sl[i].ctl, s);
+                        st_[i].htilde, s);   // its last block advances k
         }
     }
     const int fin = n_subiters & 1;
