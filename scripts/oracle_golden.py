@@ -8,6 +8,7 @@ here, and stores what the GPU tests compare against.  It calls only oracle/
 (Algorithm 1, and the SF projector) and the seeded input
 generators (synth/, via tests/problems.py); nothing comes from the CUDA path.
 
+    python scripts/oracle_golden.py c2   # 30 outer iterations (BASELINE configs[1], 2-D); full image
     python scripts/oracle_golden.py c3   # 30 outer iterations (BASELINE configs[2]); full image
     python scripts/oracle_golden.py c4   # 1 outer iteration = 24 sub-iterations (configs[3]); sampled
 
@@ -37,7 +38,7 @@ from tests.problems import config_problem, input_fingerprint, oracle_problem  # 
 
 SEED = 20240
 NSAMP = 1 << 18
-OUTER = {"c3": 30, "c4": 1}
+OUTER = {"c2": 30, "c3": 30, "c4": 1}
 
 
 def main(name):
@@ -54,7 +55,7 @@ def main(name):
     idx = np.sort(rng.choice(x.size, min(NSAMP, x.size), replace=False))
     out = dict(idx=idx, dl=pb["DL"].ravel()[idx], subiters=M * iters, threads=P.max_threads(),
                seconds=np.array([t_dl, t_run]))
-    if name == "c3":
+    if name in ("c2", "c3"):
         out["x"] = x.astype(np.float32)
     else:
         out["x"] = x.ravel()[idx]

@@ -10,6 +10,7 @@ checks the fingerprints first, so a different input set fails loudly instead
 of comparing unrelated images), the GPU computes its own D_L (ct_sqs_diag)
 and runs the solve through the C-ABI in the bench's launch path.
 
+  c2  BASELINE configs[1] (2-D fan 512^2), 30 outer iterations (1230 sub-iterations): every pixel
   c3  BASELINE configs[2], 30 outer iterations (360 sub-iterations): every voxel
   c4  BASELINE configs[3] (the 3-D helical config of the Target), one outer
       iteration (24 sub-iterations, line 1 included): the 2^18 voxels the script
@@ -67,14 +68,15 @@ def _run(C, pb, subiters):
     return rec
 
 
-def test_c3_thirty_iterations_match_oracle(C):
-    gold = _golden("c3")
-    pb = _inputs("c3", gold)
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_thirty_iterations_match_oracle(C, name):
+    gold = _golden(name)
+    pb = _inputs(name, gold)
     rec = _run(C, pb, int(gold["subiters"]))
     xg = rec.x.double().cpu().numpy()
-    xo = gold["x"].astype(np.float64)
+    xo = gold["x"].astype(np.float64).reshape(xg.shape)
     rms = math.sqrt(np.mean((xg - xo) ** 2)) / math.sqrt(np.mean(xo ** 2))
-    print("c3 after %d sub-iterations: rel RMS vs oracle %.3e" % (int(gold["subiters"]), rms))
+    print("%s after %d sub-iterations: rel RMS vs oracle %.3e" % (name, int(gold["subiters"]), rms))
     assert rms <= 1e-3, rms
     dl = rec.dl.double().cpu().numpy().ravel()[gold["idx"]]
     assert np.linalg.norm(dl - gold["dl"]) <= 1e-4 * np.linalg.norm(gold["dl"])
