@@ -182,6 +182,22 @@ ct_status ct_zprefix_size(const ct_geom* g, size_t* bytes);
 ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_views v, float* proj, void* workspace,
                              size_t workspace_bytes, ct_stream s);
 
+/* Segmented z-prefix forward (the same A x as above):
+ * the wedge of every detector-column block is walked in nseg slab segments,
+ * scheduled so that resident blocks share one xy tile of the z-prefix in L2,
+ * and the segments' raw row sums are added in segment order (deterministic)
+ * before the epilogue.  For volumes whose z-prefix array exceeds L2 (c5),
+ * where every view otherwise re-streams its band of it from HBM.
+ * nseg: -1 automatic (16 when the z-prefix array exceeds 512 MB, else off,
+ * the default), 0 or 1 off, 2..64 forced.  Applies to ct_forward_zprefix and
+ * oslalm_relaxed_solve / oslalm_profile of this geometry; it changes
+ * ct_zprefix_size and oslalm_workspace_size (query them after setting it).
+ * Frees the geometry's cached solve graphs; call it while no work of this
+ * geometry is in flight.  ct_geom_fwd_segments returns the effective count
+ * (0 = unsegmented).  Errors: CT_E_CONFIG (NULL, nseg outside [-1, 64]). */
+ct_status ct_geom_set_fwd_segments(ct_geom* g, int nseg);
+ct_status ct_geom_fwd_segments(const ct_geom* g, int* nseg);
+
 /* x_out (=|+=) scale * A' proj on views v.
  * proj: float[v.count][nt][ns]; accumulate != 0 adds into x_out. */
 ct_status ct_back(const ct_geom* g, const float* proj, ct_views v, float scale, int accumulate, float* x_out,

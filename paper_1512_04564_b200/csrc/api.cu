@@ -65,15 +65,39 @@ struct GraphKey {
     bool operator<(const GraphKey& o) const { return std::tie(ptrs, vals) < std::tie(o.ptrs, o.vals); }
 };
 
+// Schedule of the segmented forward for one (view stride, view count) (launch_fwd_seg).
+struct SegSched {
+    int2* d = nullptr;   // device entries (vi, block | segment << 16)
+    int n = 0, seg_len = 0, nseg = 0;
+};
+
 struct ct_geom {
     ct_geom_desc d;
     DGeom G;
     int device;
     float4* vtab;             // per view: cos beta, sin beta, z_s, 0
+    std::vector<float4> htab; // host copy (segmented-forward schedules)
+    int fwd_nseg = -1;        // ct_geom_set_fwd_segments: -1 automatic, 0 off, >= 2 forced
     cudaStream_t cap_stream;  // private stream for graph capture
-    std::mutex mu;            // guards the graph cache (the geometry itself is immutable)
+    std::mutex mu;            // guards the graph and schedule caches (the geometry itself is immutable)
     std::map<GraphKey, cudaGraphExec_t> graphs;
+    std::map<std::pair<int, int>, SegSched> seg;
 };
+
+// Segments of the z-prefix forward: automatic = 16 when the z-prefix array exceeds 512 MB (c5:
+// 2.2 GB; every view would otherwise re-stream its band of it from HBM), else none.
+static int fwd_nseg_of(const ct_geom* g) {
+    if (g->G.dim != 3) return 0;
+    if (g->fwd_nseg >= 0) return g->fwd_nseg >= 2 ? g->fwd_nseg : 0;
+    const double pfx = 8.0 * (double)g->G.nxy * (double)pfx_stride_of(g->G);
+    return pfx > 512.0 * 1024.0 * 1024.0 ? 16 : 0;
+}
+
+// floats of the segmented forward's partial buffer for up to `count` views (0 = unsegmented)
+static size_t fwd_part_floats(const ct_geom* g, long long count) {
+    const int ns = fwd_nseg_of(g);
+    return ns ? (size_t)ns * (size_t)count * g->G.nt * g->G.ns : 0;
+}
 
 struct ct_dist {
     ncclComm_t comm;                // NULL for a local (single-process) emulation
@@ -151,6 +175,9 @@ static ct_status validate_desc(const ct_geom_desc* d) {
     if (d->dim == 3 && (long long)d->nx * d->ny * (((long long)d->nz + 2) & ~1LL) >= (1LL << 32))
         return fail(CT_E_CONFIG, "z-prefix array of nx*ny*(nz+2) >= 2^32 entries");
     if (d->nt > 128) return fail(CT_E_CONFIG, "nt = %d > 128 detector rows", d->nt);
+    // the 3-D forward's candidate list packs a voxel column (i, j) into 16 + 16 bits
+    if (d->dim == 3 && (d->nx > 65535 || d->ny > 65535))
+        return fail(CT_E_CONFIG, "nx = %d, ny = %d: at most 65535 columns per axis in 3-D", d->nx, d->ny);
     // the update kernel keeps x+ of a 32-column tile in shared memory for the z-prefix
     if (d->nz > 1536) return fail(CT_E_CONFIG, "nz = %d > 1536 slices", d->nz);
     // source must stay outside the volume's circumscribed cylinder
@@ -235,6 +262,7 @@ extern "C" ct_status ct_geom_create(const ct_geom_desc* d, int device, ct_geom**
     }
     ct_geom* g = new ct_geom();
     g->d = *d;
+    g->htab = tab;
     g->G = make_dgeom(d);
     g->device = device;
     g->vtab = nullptr;
@@ -254,6 +282,7 @@ extern "C" void ct_geom_destroy(ct_geom* g) {
     if (!g) return;
     DeviceGuard guard(g->device);
     for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : g->seg) cudaFree(kv.second.d);
     cudaStreamDestroy(g->cap_stream);
     cudaFree(g->vtab);
     delete g;
@@ -274,6 +303,62 @@ static ct_status check_views(const ct_geom* g, ct_views v) {
 
 static Views to_views(ct_views v) { return Views{v.start, v.stride, v.count}; }
 
+// The segmented forward's schedule for views of stride `stride` (angles of start 0; the order is
+// a locality heuristic only), built and uploaded on first use -- never inside a graph capture
+// (solve_impl and ct_forward_zprefix build it before enqueueing).
+static ct_status seg_sched(const ct_geom* g, int stride, int count, const SegSched** out) {
+    ct_geom* gm = const_cast<ct_geom*>(g);
+    std::lock_guard<std::mutex> lk(gm->mu);
+    const auto key = std::make_pair(stride, count);
+    auto it = gm->seg.find(key);
+    if (it == gm->seg.end() || it->second.nseg == 0) {
+        const int nseg = fwd_nseg_of(g);
+        SegSched S;
+        std::vector<int2> h = fwd_seg_schedule(g->G, g->htab, Views{0, stride, count}, count, nseg, &S.seg_len);
+        S.n = (int)h.size();
+        S.nseg = (std::max(g->G.nx, g->G.ny) + S.seg_len - 1) / S.seg_len;
+        CT_CUDA(cudaMalloc(&S.d, sizeof(int2) * h.size()));
+        CT_CUDA(cudaMemcpy(S.d, h.data(), sizeof(int2) * h.size(), cudaMemcpyHostToDevice));
+        it = gm->seg.emplace(key, S).first;
+    }
+    *out = &it->second;
+    return CT_OK;
+}
+
+// z-prefix forward of `max_count` views (from ctl, or v), segmented when fwd_nseg_of(g) > 0 (part:
+// the partial buffer, fwd_part_floats(g, max_count) floats; the schedule must exist already).
+static void fwd_pfx(const ct_geom* g, const Ctl* ctl, Views v, int sched_stride, int max_count, const float* xt,
+                    const float* y, const float* w, float* out, int mode, float* part, cudaStream_t s) {
+    if (fwd_nseg_of(g) && part) {
+        const auto it = g->seg.find(std::make_pair(sched_stride, max_count));
+        const SegSched& S = it->second;
+        launch_fwd_seg(g->G, g->vtab, ctl, v, max_count, xt, y, w, out, mode, s, pfx_stride_of(g->G), S.d, S.n,
+                       S.seg_len, S.nseg, part);
+    } else {
+        launch_fwd(g->G, g->vtab, ctl, v, max_count, xt, xt, y, w, out, mode, s, pfx_stride_of(g->G));
+    }
+}
+
+extern "C" ct_status ct_geom_set_fwd_segments(ct_geom* g, int nseg) {
+    if (!g) return fail(CT_E_CONFIG, "ct_geom_set_fwd_segments: NULL geometry");
+    if (nseg < -1 || nseg > 64) return fail(CT_E_CONFIG, "nseg = %d outside [-1, 64]", nseg);
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->fwd_nseg = nseg;
+    DeviceGuard guard(g->device);
+    cudaDeviceSynchronize();   // no launch may still read a schedule or graph freed below
+    for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second);
+    g->graphs.clear();
+    for (auto& kv : g->seg) cudaFree(kv.second.d);
+    g->seg.clear();
+    return CT_OK;
+}
+
+extern "C" ct_status ct_geom_fwd_segments(const ct_geom* g, int* nseg) {
+    if (!g || !nseg) return fail(CT_E_CONFIG, "ct_geom_fwd_segments: NULL argument");
+    *nseg = fwd_nseg_of(g);
+    return CT_OK;
+}
+
 // ------------------------------------------------------------------ projector
 extern "C" ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, float* proj, ct_stream s) {
     if (!g || !x || !proj) return fail(CT_E_CONFIG, "ct_forward: NULL argument");
@@ -285,9 +370,16 @@ extern "C" ct_status ct_forward(const ct_geom* g, const float* x, ct_views v, fl
     return check_async();
 }
 
+// views per launch of a segmented ct_forward_zprefix (its partial buffer is sized for these)
+constexpr int kZpfxChunk = 128;
+
+static size_t zprefix_bytes(const ct_geom* g) {
+    return g->G.dim == 3 ? align_up(sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G)) : 0;
+}
+
 extern "C" ct_status ct_zprefix_size(const ct_geom* g, size_t* bytes) {
     if (!g || !bytes) return fail(CT_E_CONFIG, "ct_zprefix_size: NULL argument");
-    *bytes = g->G.dim == 3 ? sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G) : 0;
+    *bytes = g->G.dim == 3 ? zprefix_bytes(g) + sizeof(float) * fwd_part_floats(g, std::min(kZpfxChunk, g->d.na)) : 0;
     return CT_OK;
 }
 
@@ -305,8 +397,21 @@ extern "C" ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_vie
     DeviceGuard guard(g->device);
     float* pfx = (float*)workspace;
     launch_zprefix(g->G, x, pfx, (cudaStream_t)s);
-    launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, pfx, pfx, nullptr, nullptr, proj, FWD_PLAIN,
-               (cudaStream_t)s, pfx_stride_of(g->G));
+    if (!fwd_nseg_of(g)) {
+        launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, pfx, pfx, nullptr, nullptr, proj, FWD_PLAIN,
+                   (cudaStream_t)s, pfx_stride_of(g->G));
+        return check_async();
+    }
+    // segmented: chunks of kZpfxChunk views through the partial buffer after the z-prefix
+    float* part = (float*)((char*)workspace + zprefix_bytes(g));
+    for (int c0 = 0; c0 < v.count; c0 += kZpfxChunk) {
+        const int cnt = std::min(kZpfxChunk, v.count - c0);
+        const SegSched* S;
+        st = seg_sched(g, v.stride, cnt, &S);
+        if (st != CT_OK) return st;
+        fwd_pfx(g, nullptr, Views{v.start + c0 * v.stride, v.stride, cnt}, v.stride, cnt, pfx, nullptr, nullptr,
+                proj + (size_t)c0 * g->G.nt * g->G.ns, FWD_PLAIN, part, (cudaStream_t)s);
+    }
     return check_async();
 }
 
@@ -431,7 +536,7 @@ extern "C" ct_status ct_reg_grad(const ct_geom* g, const ct_reg_desc* r, const f
 
 // ------------------------------------------------------------------ solver
 struct WsLayout {
-    size_t ctl, xalt, xt, r, r_stride, zeta, zeta_stride, gradr, curvr, flag, dsum, total;
+    size_t ctl, xalt, xt, part, r, r_stride, zeta, zeta_stride, gradr, curvr, flag, dsum, total;
 };
 
 
@@ -448,6 +553,8 @@ static WsLayout ws_layout(const ct_geom* g, const oslalm_params* p, const ct_dis
     off = align_up(off + sizeof(float) * g->G.nvox);
     L.xt = off;  // z-prefix array of x+ for the 3-D forward projector
     if (g->G.dim == 3) off = align_up(off + sizeof(float2) * (size_t)g->G.nxy * pfx_stride_of(g->G));
+    L.part = off;  // segmented forward: raw segment sums of one rank's views (fwd_part_floats)
+    off = align_up(off + sizeof(float) * fwd_part_floats(g, vrank));
     L.r = off;     // residual of each local rank's views
     L.r_stride = align_up(sizeof(float) * (size_t)vrank * g->G.nt * g->G.ns);
     off += L.r_stride * nl;
@@ -500,9 +607,9 @@ extern "C" double oslalm_rho(int64_t k, double alpha) {
 static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, float* xa, float* xb, float* xt,
                             const float* y, const float* w, const float* dl, float* gb, float* ht,
                             const float* kappa, float* r, int max_count, float M, float lo, float hi,
-                            cudaStream_t s) {
+                            float* part, cudaStream_t s) {
     launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, xt, s);
-    if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, r, FWD_RESID, s, pfx_stride_of(g->G));
+    if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, (int)M, max_count, xt, y, w, r, FWD_RESID, part, s);
     else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
     launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);   // + k advance
 }
@@ -532,6 +639,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     float* xalt = (float*)(ws + L.xalt);
     float* xt = g->G.dim == 3 ? (float*)(ws + L.xt) : nullptr;
     float* rbuf = (float*)(ws + L.r);
+    float* part = (float*)(ws + L.part);   // segmented forward (fwd_nseg_of)
     float* zeta = dist ? (float*)(ws + L.zeta) : nullptr;
     const int nl = local_ranks(dist);
     const long long zstride = (long long)(L.zeta_stride / sizeof(float)), rstride = (long long)(L.r_stride / sizeof(float));
@@ -548,6 +656,12 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     if ((long long)max_count * g->G.nt * g->G.ns >= (1LL << 31))
         return fail(CT_E_SHAPE, "subset projection block exceeds 2^31 elements (increase M)");
     const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
+    const int sstride = world * M;   // view stride of a rank's subset (the segmented forward's schedule)
+    if (xt && fwd_nseg_of(g)) {
+        const SegSched* S;
+        ct_status e = seg_sched(g, sstride, max_count, &S);
+        if (e != CT_OK) return e;
+    }
 
     std::vector<Ctl> hctl(nl);
     for (int q = 0; q < nl; q++) {
@@ -620,7 +734,8 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                     (uintptr_t)d_l, (uintptr_t)st->g, (uintptr_t)st->htilde, (uintptr_t)kappa, (uintptr_t)rbuf,
                     (uintptr_t)xt};
         key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi, (double)p->variant,
-                    (double)rp.potential, (double)rp.delta, (double)rp.n_dirs, (double)rp.maxcurv, (double)rp.q};
+                    (double)rp.potential, (double)rp.delta, (double)rp.n_dirs, (double)rp.maxcurv, (double)rp.q,
+                    (double)fwd_nseg_of(g)};
         for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
         std::lock_guard<std::mutex> lk(const_cast<ct_geom*>(g)->mu);
         auto it = g->graphs.find(key);
@@ -630,7 +745,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             cudaStream_t cs = g->cap_stream;
             CT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
             enqueue_subiter(g, rp, ctl, st->x, xalt, xt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count, Mf,
-                            lo, hi, cs);
+                            lo, hi, part, cs);
             cudaGraph_t graph;
             cudaError_t e = cudaStreamEndCapture(cs, &graph);
             if (e != cudaSuccess) return fail(CT_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -703,8 +818,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
-            if (xt) launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xt, xt, y, w, rbuf, FWD_RESID, s,
-                               pfx_stride_of(g->G));
+            if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, sstride, max_count, xt, y, w, rbuf, FWD_RESID, part, s);
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
             launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g, st->htilde, s);
@@ -760,8 +874,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             }
             for (int q = 0; q < nl; q++) {
                 float* rq = rbuf + q * rstride;
-                if (xt) launch_fwd(G, g->vtab, ctl + q, Views{0, 1, 0}, max_count, xt, xt, y, w, rq, FWD_RESID, s,
-                                   pfx_stride_of(G));
+                if (xt) fwd_pfx(g, ctl + q, Views{0, 1, 0}, sstride, max_count, xt, y, w, rq, FWD_RESID, part, s);
                 else launch_fwd(G, g->vtab, ctl + q, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rq, FWD_RESID, s);
             }
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));

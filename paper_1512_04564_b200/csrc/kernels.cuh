@@ -1,5 +1,7 @@
 // kernels.cuh — host-side launcher declarations for libctrecon.so kernels.
 #pragma once
+#include <vector>
+
 #include "ct_internal.cuh"
 
 namespace ctr {
@@ -21,6 +23,17 @@ struct RegParams {
 void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* xa,
                 const float* xb, const float* y, const float* w, float* out, int mode, cudaStream_t s,
                 int pfx_stride = 0);  // > 0: xa is the float2 z-prefix array (3-D solve path)
+
+// Segmented z-prefix forward (volumes whose z-prefix exceeds L2): nseg segments of
+// seg_len slabs along each wedge; sched from fwd_seg_schedule (device copy, nsched entries); part =
+// nseg * max_count * nt * ns floats of raw segment sums, reduced in segment order into out with the
+// forward's epilogue (mode as launch_fwd).
+int fwd_seg_len(const DGeom& G, int nseg);
+std::vector<int2> fwd_seg_schedule(const DGeom& G, const std::vector<float4>& htab, Views v, int count, int nseg,
+                                   int* seg_len);
+void launch_fwd_seg(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* pfx,
+                    const float* y, const float* w, float* out, int mode, cudaStream_t s, int pfx_stride,
+                    const int2* sched, int nsched, int seg_len, int nseg, float* part);
 
 // z-prefix array of x+ for the 3-D forward (written by the update kernel):
 // per voxel column, float2 Q_k = (A_k, x_k) for k = 0..nz-1 and Q_nz = (P_nz, 0),

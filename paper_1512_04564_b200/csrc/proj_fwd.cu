@@ -12,6 +12,7 @@
 //   FWD_ONES_W r = L_z w (L_z A0 1)      (D_L = A'WA1)
 #include <algorithm>
 #include <cmath>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -232,6 +233,9 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
                  : "memory");
 }
 
+#ifndef F3_CREDIT2
+#define F3_CREDIT2 0   // a hit's credits to the 4 detector columns as packed FP32 pairs (FFMA2)
+#endif
 #ifndef F3_WCSMEM
 #define F3_WCSMEM 1    // the candidate walk's per-warp constants in shared memory (frees registers)
 #endif
@@ -261,11 +265,17 @@ __device__ __forceinline__ int fwd_row(int lane, int r) { return F3_STRIDED ? la
 #endif
 // NW warps per block (4, or 2 for small grids: finer blocks shorten the last wave); 32 / NW
 // blocks per SM keep the same 32 resident warps at 64 registers
-template <bool ARC, int MODE, int RPL, bool PFX, int NW>
+// SEG (segmented forward, c5-sized volumes whose z-prefix exceeds L2): block b
+// takes its (view, detector-column block, segment) from sched[b] -- entries sorted by the xy tile
+// the segment's piece of the wedge crosses, so that resident blocks share a tile's z-prefix in
+// L2 -- walks only the segment's slabs [seg * seg_len, (seg + 1) * seg_len) and writes its raw row
+// sums to part[seg][vi][t][s]; k_fwd3_reduce adds the segments in order and applies the epilogue.
+template <bool ARC, int MODE, int RPL, bool PFX, int NW, bool SEG = false>
 __global__ void __launch_bounds__(32 * NW, F3_MINB * F3_NWARPS / NW)
 k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
-       const float* __restrict__ w, float* __restrict__ out, int pfx_stride, int slot_entries) {
+       const float* __restrict__ w, float* __restrict__ out, int pfx_stride, int slot_entries,
+       const int2* __restrict__ sched, int seg_len, int part_views) {
     constexpr bool TMA = PFX && F3_TMA;
     constexpr int TD = F3_TMAD;
     extern __shared__ __align__(16) float2 fwd_ring[];   // TMA: [NW][TD][slot_entries]
@@ -284,10 +294,16 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     constexpr bool ONES = (MODE == FWD_ONES_W);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const Views V = select_views(ctl, vsel);
-    const int vi = blockIdx.y;
+    int vi = blockIdx.y, bxi = blockIdx.x, seg = 0;
+    if (SEG) {
+        const int2 e = __ldg(&sched[blockIdx.x]);
+        vi = e.x;
+        bxi = e.y & 0xffff;
+        seg = e.y >> 16;
+    }
     if (vi >= V.count) return;
     const int v = V.start + vi * V.stride;
-    const int sb0 = blockIdx.x * (NW * F3_CPW);          // first detector column of the block
+    const int sb0 = bxi * (NW * F3_CPW);          // first detector column of the block
     const int s0 = sb0 + wid * F3_CPW;             // first detector column of the warp
     const float* __restrict__ x = xa;
     if (ctl && !PFX) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
@@ -305,16 +321,26 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
         __syncwarp();
     }
 
+#if F3_CREDIT2
+    // row sums of detector columns (0, 1) and (2, 3) as packed pairs: a hit's credits are 2 RPL
+    // FFMA2 (L4.xy / L4.zw times the broadcast row sum) instead of 4 RPL FFMA
+    float2 acc2[2][RPL];
+#pragma unroll
+    for (int c = 0; c < 2; c++)
+#pragma unroll
+        for (int r = 0; r < RPL; r++) acc2[c][r] = make_float2(0.f, 0.f);
+#else
     float acc[F3_CPW][RPL];
 #pragma unroll
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
         for (int r = 0; r < RPL; r++) acc[c][r] = 0.f;
+#endif
 
 #if F3_PREYW
     // y and w of the block's (row, column) outputs are read only by the epilogue: start their
     // copies into shared memory now (cp.async) so that the epilogue does not wait on HBM
-    constexpr bool YW = (MODE != FWD_PLAIN);
+    constexpr bool YW = (MODE != FWD_PLAIN) && !SEG;
     if (YW) {
         for (int q = threadIdx.x; q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
             const int t = q / (NW * F3_CPW), c = q % (NW * F3_CPW);
@@ -388,10 +414,14 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #define WCX(v) (v)
 #endif
 
-        for (int sl0 = 0; sl0 < WCX(na_); sl0 += 32 / F3_SUB) {
+        // the segment's slabs (SEG); otherwise every slab, the bound re-read from shared memory
+        const int slb = SEG ? seg * seg_len : 0;
+        const int sle_seg = SEG ? min(WCX(na_), slb + seg_len) : 0;
+#define SLE (SEG ? sle_seg : WCX(na_))
+        for (int sl0 = slb; sl0 < SLE; sl0 += 32 / F3_SUB) {
             const int sl = sl0 + lane / F3_SUB, sub = lane % F3_SUB;
             int lo = 0, hi = -1;
-            if (sl < WCX(na_)) {
+            if (sl < SLE) {
                 const float ac = fmaf((float)sl, WCX(da), WCX(a0));
                 const float pa = ac - WCX(ha) - WCX(Sa), pb = ac + WCX(ha) - WCX(Sa);
                 if (pa * WCX(sgn) > 0.f && pb * WCX(sgn) > 0.f) {
@@ -587,10 +617,15 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                     }
 #pragma unroll
                     for (int r = 0; r < RPL; r++) {
+#if F3_CREDIT2
+                        acc2[0][r] = fma2(make_float2(L4.x, L4.y), bcast2(Rs[r]), acc2[0][r]);
+                        acc2[1][r] = fma2(make_float2(L4.z, L4.w), bcast2(Rs[r]), acc2[1][r]);
+#else
                         acc[0][r] = fmaf(L4.x, Rs[r], acc[0][r]);
                         acc[1][r] = fmaf(L4.y, Rs[r], acc[1][r]);
                         acc[2][r] = fmaf(L4.z, Rs[r], acc[2][r]);
                         acc[3][r] = fmaf(L4.w, Rs[r], acc[3][r]);
+#endif
                     }
                 }
                 if (TMA) tcnt += n;
@@ -600,16 +635,31 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 
 #undef WCX
+#undef SLE
     // epilogue: stage [row][detector column in block], then each thread handles one (row, column)
 #pragma unroll
     for (int c = 0; c < F3_CPW; c++)
 #pragma unroll
-        for (int r = 0; r < RPL; r++) stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c] = acc[c][r];
+        for (int r = 0; r < RPL; r++)
+#if F3_CREDIT2
+            stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c] = (c & 1) ? acc2[c >> 1][r].y : acc2[c >> 1][r].x;
+#else
+            stage[fwd_row<RPL>(lane, r)][wid * F3_CPW + c] = acc[c][r];
+#endif
 #if F3_PREYW
     if (YW) asm volatile("cp.async.wait_all;" ::: "memory");
 #endif
     __syncthreads();
-    for (int q = threadIdx.x; q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
+    if (SEG) {
+        // raw row sums of this segment (L_z, w and y are applied by k_fwd3_reduce)
+        float* __restrict__ pp = out + (size_t)(seg * part_views + vi) * G.nt * G.ns;
+        for (int q = threadIdx.x; q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
+            const int t = q / (NW * F3_CPW), c = q % (NW * F3_CPW);
+            const int ss = sb0 + c;
+            if (ss < G.ns) __stcg(pp + (size_t)t * G.ns + ss, stage[t][c]);
+        }
+    }
+    for (int q = threadIdx.x; !SEG && q < G.nt * (NW * F3_CPW); q += (32 * NW)) {
         const int t = q / (NW * F3_CPW), c = q % (NW * F3_CPW);
         const int ss = sb0 + c;
         if (ss >= G.ns) continue;
@@ -651,7 +701,8 @@ static void fwd3_launch(const DGeom& G, dim3 grid, const float4* vtab, const Ctl
     const size_t smem = (size_t)NW * F3_TMAD * se * sizeof(float2);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_fwd3<ARC, MODE, RPL, PFX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_fwd3<ARC, MODE, RPL, PFX, NW><<<grid, 32 * NW, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps, se);
+    k_fwd3<ARC, MODE, RPL, PFX, NW>
+        <<<grid, 32 * NW, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps, se, nullptr, 0, 0);
 }
 
 template <bool ARC, int MODE, bool PFX, int NW>
@@ -732,6 +783,137 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
         else fwd2_dispatch<false>(G, vtab, ctl, v, max_count, xa, xb, y, w, out, mode, s);
     }
     launches_add(1);
+}
+
+
+// ---------------------------------------------------------------------------
+// Segmented z-prefix forward (SEG above).  The segment length is a multiple of the 32-slab pass
+// so that segments split no pass; the schedule is built on the host from the view table.
+int fwd_seg_len(const DGeom& G, int nseg) {
+    const int na = std::max(G.nx, G.ny);
+    const int per = (na + nseg - 1) / nseg;
+    return ((per + 31) / 32) * 32;
+}
+
+// Schedule of the segmented forward for views {start + vi stride}, vi < count: every
+// (vi, detector-column block, segment) once, sorted by the xy tile (serpentine order) that the
+// middle ray of the block crosses at the middle of the segment, then by view -- resident blocks
+// then work on one tile's voxel columns (a tile's z-prefix fits L2) across consecutive views.
+std::vector<int2> fwd_seg_schedule(const DGeom& G, const std::vector<float4>& htab, Views v, int count, int nseg,
+                                   int* seg_len_out) {
+    const int seg_len = fwd_seg_len(G, nseg);
+    const int nseg_eff = (std::max(G.nx, G.ny) + seg_len - 1) / seg_len;
+    const int cpb = F3_NWARPS * F3_CPW;
+    const int nbx = (G.ns + cpb - 1) / cpb;
+    // tile edge (voxels): about 32 MB of z-prefix per tile, a power of two in [32, 256]
+    const double per_col = 8.0 * (double)pfx_stride_of(G);
+    int T = 32;
+    while (T < 256 && (double)(2 * T) * (2 * T) * per_col <= 32.0 * 1024 * 1024) T *= 2;
+    const int ntx = (G.nx + T - 1) / T, nty = (G.ny + T - 1) / T;
+    struct E {
+        long long key;
+        int2 e;
+    };
+    std::vector<E> ent;
+    ent.reserve((size_t)count * nbx * nseg_eff);
+    for (int vi = 0; vi < count; vi++) {
+        const float4 vw = htab[(size_t)v.start + (size_t)vi * v.stride];
+        const double cb = vw.x, sb = vw.y;
+        const double Sx = G.dso * cb, Sy = G.dso * sb;
+        for (int bx = 0; bx < nbx; bx++) {
+            const double sm = std::min(bx * cpb + cpb / 2, G.ns - 1);
+            const double tm = (sm - G.s_c0) * G.delta;
+            const double cam = G.arc ? std::cos(tm) : G.dsd, cum = G.arc ? std::sin(tm) : tm;
+            const double dmx = -cam * cb - cum * sb, dmy = -cam * sb + cum * cb;
+            const bool xstep = std::fabs(dmx) >= std::fabs(dmy);
+            for (int sg = 0; sg < nseg_eff; sg++) {
+                const int na_ = xstep ? G.nx : G.ny;
+                const double slab = std::min((double)sg * seg_len + 0.5 * seg_len, (double)na_ - 0.5);
+                const double a = (xstep ? G.x0 : G.y0) + slab * (xstep ? G.dx : G.dy);
+                const double lam = (a - (xstep ? Sx : Sy)) / (xstep ? dmx : dmy);
+                const double o = (xstep ? Sy : Sx) + lam * (xstep ? dmy : dmx);
+                const double px = xstep ? a : o, py = xstep ? o : a;
+                int tx = (int)std::floor((px - G.x0) / G.dx / T + 0.5 / T);
+                int ty = (int)std::floor((py - G.y0) / G.dy / T + 0.5 / T);
+                tx = std::min(std::max(tx, 0), ntx - 1);
+                ty = std::min(std::max(ty, 0), nty - 1);
+                const long long tile = (long long)ty * ntx + ((ty & 1) ? ntx - 1 - tx : tx);
+                const long long key = ((tile * count + vi) * nseg_eff + sg) * nbx + bx;
+                ent.push_back(E{key, make_int2(vi, bx | (sg << 16))});
+            }
+        }
+    }
+    std::stable_sort(ent.begin(), ent.end(), [](const E& p, const E& q) { return p.key < q.key; });
+    std::vector<int2> out(ent.size());
+    for (size_t q = 0; q < ent.size(); q++) out[q] = ent[q].e;
+    *seg_len_out = seg_len;
+    return out;
+}
+
+// Sum of the segments' raw row sums in segment order (deterministic) + the forward's epilogue.
+template <bool ARC, int MODE>
+__global__ void __launch_bounds__(256) k_fwd3_reduce(DGeom G, const Ctl* __restrict__ ctl, Views vsel,
+                                                     const float* __restrict__ part, int nseg, int part_views,
+                                                     const float* __restrict__ y, const float* __restrict__ w,
+                                                     float* __restrict__ out) {
+    const Views V = select_views(ctl, vsel);
+    const long long per = (long long)G.nt * G.ns;
+    const long long n = (long long)V.count * per, pstride = (long long)part_views * per;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        float acc = __ldcs(part + q);
+        for (int sg = 1; sg < nseg; sg++) acc += __ldcs(part + q + sg * pstride);
+        const int ss = (int)(q % G.ns), t = (int)((q / G.ns) % G.nt);
+        const long long vi = q / per;
+        const float lz = ray_Lz<ARC>(G, ss, t);
+        const float p = lz * acc;
+        if (MODE == FWD_PLAIN) {
+            out[q] = p;
+        } else {
+            const size_t a = ((size_t)(V.start + vi * V.stride) * G.nt + t) * G.ns + ss;
+            const float wv = w ? __ldcs(&w[a]) : 1.f;
+            if (MODE == FWD_RESID) out[q] = lz * wv * (p - __ldcs(&y[a]));
+            else out[q] = lz * wv * p;
+        }
+    }
+}
+
+template <bool ARC, int RPL, int NW>
+static void fwd3_seg_launch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* pfx,
+                            int ps, const int2* sched, int nsched, int seg_len, int max_count, float* part,
+                            cudaStream_t s) {
+    k_fwd3<ARC, FWD_PLAIN, RPL, true, NW, true><<<nsched, 32 * NW, 0, s>>>(
+        G, vtab, ctl, v, pfx, pfx, nullptr, nullptr, part, ps, 0, sched, seg_len, max_count);
+}
+
+void launch_fwd_seg(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count, const float* pfx,
+                    const float* y, const float* w, float* out, int mode, cudaStream_t s, int pfx_stride,
+                    const int2* sched, int nsched, int seg_len, int nseg, float* part) {
+    if (max_count <= 0) return;
+    constexpr int NW = F3_NWARPS;
+#define CTR_SEG(ARC)                                                                                          \
+    if (G.nt <= 32) fwd3_seg_launch<ARC, 1, NW>(G, vtab, ctl, v, pfx, pfx_stride, sched, nsched, seg_len, max_count, part, s); \
+    else if (G.nt <= 64) fwd3_seg_launch<ARC, 2, NW>(G, vtab, ctl, v, pfx, pfx_stride, sched, nsched, seg_len, max_count, part, s); \
+    else fwd3_seg_launch<ARC, 4, NW>(G, vtab, ctl, v, pfx, pfx_stride, sched, nsched, seg_len, max_count, part, s);
+    if (G.arc) {
+        CTR_SEG(true)
+    } else {
+        CTR_SEG(false)
+    }
+#undef CTR_SEG
+    const long long n = (long long)max_count * G.nt * G.ns;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+#define CTR_RED(ARC)                                                                                               \
+    if (mode == FWD_PLAIN) k_fwd3_reduce<ARC, FWD_PLAIN><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out); \
+    else if (mode == FWD_RESID) k_fwd3_reduce<ARC, FWD_RESID><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out); \
+    else k_fwd3_reduce<ARC, FWD_ONES_W><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out);
+    if (G.arc) {
+        CTR_RED(true)
+    } else {
+        CTR_RED(false)
+    }
+#undef CTR_RED
+    launches_add(2);
 }
 
 }  // namespace ctr

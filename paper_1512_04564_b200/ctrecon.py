@@ -70,7 +70,7 @@ EXPORTS = ["ct_geom_create", "ct_geom_destroy", "ct_forward", "ct_back", "ct_sqs
            "ct_nccl_unique_id", "ct_dist_create", "ct_dist_destroy", "ct_launch_count", "ct_last_error",
            "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size", "ct_sqs_diag_zslab",
            "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size", "ct_forward_zprefix",
-           "oslalm_residual", "ct_dist_create_local"]
+           "oslalm_residual", "ct_dist_create_local", "ct_geom_set_fwd_segments", "ct_geom_fwd_segments"]
 
 _lib = None
 
@@ -91,6 +91,8 @@ def load():
     L.ct_back.argtypes = [vp, vp, ct_views, f, ctypes.c_int, vp, vp]
     L.ct_zprefix_size.argtypes = [vp, P(ctypes.c_size_t)]
     L.ct_forward_zprefix.argtypes = [vp, vp, ct_views, vp, vp, ctypes.c_size_t, vp]
+    L.ct_geom_set_fwd_segments.argtypes = [vp, ctypes.c_int]
+    L.ct_geom_fwd_segments.argtypes = [vp, P(ctypes.c_int)]
     L.oslalm_residual.argtypes = [vp, P(oslalm_params), vp, ctypes.c_int64, vp, ctypes.c_size_t, vp, vp]
     L.ct_sqs_diag.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.ct_reg_grad.argtypes = [vp, P(ct_reg_desc), vp, vp, vp, vp, vp]
@@ -125,7 +127,8 @@ def load():
                  "oslalm_relaxed_solve", "oslalm_state_h", "ct_sync", "ct_nccl_unique_id", "ct_dist_create",
                  "oslalm_profile", "ct_count_nnz", "ct_zslab_range", "oslalm_zslab_workspace_size",
                  "ct_sqs_diag_zslab", "oslalm_zslab_solve", "ct_sino_upload", "ct_count_work", "ct_zprefix_size",
-                 "ct_forward_zprefix", "oslalm_residual", "ct_dist_create_local"):
+                 "ct_forward_zprefix", "oslalm_residual", "ct_dist_create_local", "ct_geom_set_fwd_segments",
+                 "ct_geom_fwd_segments"):
         getattr(L, name).restype = st
     _lib = L
     return L
@@ -209,6 +212,16 @@ def ct_zprefix_size(geom):
 def ct_forward_zprefix(geom, x, v, proj, workspace, stream=None):
     _check(load().ct_forward_zprefix(geom, _ptr(x), v, _ptr(proj), ctypes.c_void_p(workspace.data_ptr()),
                                      workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def ct_geom_set_fwd_segments(geom, nseg):
+    _check(load().ct_geom_set_fwd_segments(geom, int(nseg)))
+
+
+def ct_geom_fwd_segments(geom):
+    n = ctypes.c_int()
+    _check(load().ct_geom_fwd_segments(geom, ctypes.byref(n)))
+    return n.value
 
 
 def oslalm_residual(geom, p, k, workspace, r_out, dist=None, stream=None):

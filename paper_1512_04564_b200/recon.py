@@ -21,14 +21,18 @@ def _variant(solver):
 
 
 class Recon:
-    def __init__(self, geom, reg, solver, y, w, x0, kappa=None, device=0, dist=None, stream=None):
+    def __init__(self, geom, reg, solver, y, w, x0, kappa=None, device=0, dist=None, stream=None,
+                 fwd_segments=None):
         """geom/reg/solver: dicts as in synth/configs.py; y, w: (na, nt, ns);
         x0: (nz, ny, nx).  Arrays may be numpy/torch of any float dtype; they
-        are copied to float32 device tensors."""
+        are copied to float32 device tensors.  fwd_segments: None = the library's
+        automatic choice, else ct_geom_set_fwd_segments(nseg) (0 = off)."""
         self.dev = torch.device("cuda", device)
         self.geom = geom
         self.desc = C.geom_desc(geom)
         self.h = C.ct_geom_create(self.desc, device)
+        if fwd_segments is not None:
+            C.ct_geom_set_fwd_segments(self.h, fwd_segments)
         self.dist = dist
         self.stream = stream
         f32 = dict(dtype=torch.float32, device=self.dev)

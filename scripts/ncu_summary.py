@@ -70,7 +70,7 @@ def main():
     # the solve's sub-iteration kernels: update, forward with the residual epilogue (MODE 1), back with
     # the g/htilde epilogue (EPI 3), advance
     sub = {k: v for k, v in agg.items() if k.startswith(("k_update<", "k_advance")) or
-           re.fullmatch(r"k_fwd3<\d,1,\d,1(?:,\d)?>|k_fwd2<\d,1>|k_back3<\d,3,0,\d+>|k_back2<\d,3,\d>", k)}
+           re.fullmatch(r"k_fwd3<\d,[01],\d,1(?:,\d)*>|k_fwd3_reduce<\d,1>|k_fwd2<\d,1>|k_back3<\d,3,0,\d+>|k_back2<\d,3,\d>", k)}
     tot = sum(v[1] for v in sub.values())
     lines = ["# ncu summary %s" % tag, "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "

@@ -134,3 +134,80 @@ def test_mid_solve_trace_and_residual(C, kind):
         err = np.linalg.norm(host(r) - ro) / np.linalg.norm(wm * ax)
         assert err <= 1e-4, (k, err)
     rec.close()
+
+
+@pytest.mark.parametrize("kind,nseg", [("helical_mid", 3), ("helical_rpl4", 2), ("axial_mid", 5),
+                                       ("helical_thin", 4)])
+def test_segmented_forward_parity(C, kind, nseg):
+    """The segmented z-prefix forward (ct_geom_set_fwd_segments; automatic for c5-sized
+    volumes): the wedge walked in nseg slab segments, tile-ordered blocks, segment sums
+    added in order.  Against the oracle over all views (chunks of 128 views when na > 128)
+    and a strided subset, against the unsegmented forward, and bitwise repeatable."""
+    g = mid(kind)
+    na = g["na"]
+    rng = np.random.default_rng(41)
+    x = rng.random(P.vol_shape(g))
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        assert C.ct_geom_fwd_segments(h) == 0      # mid-size volumes: automatic = off
+        xd = dev(x)
+        ws0 = torch.empty(C.ct_zprefix_size(h), dtype=torch.uint8, device="cuda")
+        p0 = torch.empty(P.proj_shape(g, na), dtype=torch.float32, device="cuda")
+        C.ct_forward_zprefix(h, xd, C.views(0, 1, na), p0, ws0)
+        C.ct_geom_set_fwd_segments(h, nseg)
+        assert C.ct_geom_fwd_segments(h) == nseg
+        ws = torch.empty(C.ct_zprefix_size(h), dtype=torch.uint8, device="cuda")
+        assert ws.numel() > ws0.numel()
+        ps = torch.empty_like(p0)
+        C.ct_forward_zprefix(h, xd, C.views(0, 1, na), ps, ws)
+        ref = P.forward(g, x)
+        assert rel(host(ps), ref) <= 1e-4, rel(host(ps), ref)
+        assert rel(host(ps), host(p0)) <= 1e-5
+        ps2 = torch.empty_like(p0)
+        C.ct_forward_zprefix(h, xd, C.views(0, 1, na), ps2, ws)
+        assert torch.equal(ps, ps2)
+        vv = (2, 3, (na - 2 + 2) // 3)
+        pv = torch.empty(P.proj_shape(g, vv[2]), dtype=torch.float32, device="cuda")
+        C.ct_forward_zprefix(h, xd, C.views(*vv), pv, ws)
+        assert rel(host(pv), P.forward(g, x, vv)) <= 1e-4
+        C.ct_geom_set_fwd_segments(h, -1)
+        assert C.ct_geom_fwd_segments(h) == 0
+    finally:
+        C.ct_geom_destroy(h)
+
+
+@pytest.mark.parametrize("kind,nseg", [("helical_mid", 3), ("helical_rpl4", 4)])
+def test_segmented_solve_trace(C, kind, nseg):
+    """Algorithm 1 (M = 2) with the segmented forward in the graph-replayed solve:
+    x, g, htilde against the oracle's trace and the solver's residual against
+    W_m (A_m x+ - y_m) of the oracle, as test_mid_solve_trace_and_residual."""
+    from paper_1512_04564_b200.recon import Recon
+    g = mid(kind)
+    M = 2
+    pb = synthetic_problem(g, M=M)
+    prob = oracle_problem(pb)
+    DL = pb["DL"]
+    trace = {}
+    alg.alg1(prob, pb["x0"], M, 1.999, 3, DL=DL, trace=trace)
+    rec = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], fwd_segments=nseg)
+    assert C.ct_geom_fwd_segments(rec.h) == nseg
+    rec.set_DL(DL)
+    done = 0
+    na = g["na"]
+    for k in (1, 3, 5):
+        rec.run(k - done)
+        done = k
+        xo, go, ho = trace[k]
+        assert rel(host(rec.x), xo) <= 1e-4, (k, rel(host(rec.x), xo))
+        assert rel(host(rec.g), go) <= 1e-3, (k, rel(host(rec.g), go))
+        assert rel(host(rec.htilde), DL * xo - ho) <= 1e-3, k
+        m = (k - 1) % M
+        views = alg.subset_views(na, M, m)
+        r = torch.empty(P.proj_shape(g, views[2]), dtype=torch.float32, device="cuda")
+        C.oslalm_residual(rec.h, rec.params, k, rec.ws, r)
+        ax = P.forward(g, xo, views)
+        wm = alg.subset_rows(pb["w"], na, M, m)
+        ro = wm * (ax - alg.subset_rows(pb["y"], na, M, m))
+        err = np.linalg.norm(host(r) - ro) / np.linalg.norm(wm * ax)
+        assert err <= 1e-4, (k, err)
+    rec.close()
