@@ -789,6 +789,9 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
 // ---------------------------------------------------------------------------
 // Segmented z-prefix forward (SEG above).  The segment length is a multiple of the 32-slab pass
 // so that segments split no pass; the schedule is built on the host from the view table.
+#ifndef FWD_SEG_TILE_MB
+#define FWD_SEG_TILE_MB 32   // z-prefix bytes per schedule tile (c5: 64 x 64 columns)
+#endif
 int fwd_seg_len(const DGeom& G, int nseg) {
     const int na = std::max(G.nx, G.ny);
     const int per = (na + nseg - 1) / nseg;
@@ -805,10 +808,10 @@ std::vector<int2> fwd_seg_schedule(const DGeom& G, const std::vector<float4>& ht
     const int nseg_eff = (std::max(G.nx, G.ny) + seg_len - 1) / seg_len;
     const int cpb = F3_NWARPS * F3_CPW;
     const int nbx = (G.ns + cpb - 1) / cpb;
-    // tile edge (voxels): about 32 MB of z-prefix per tile, a power of two in [32, 256]
+    // tile edge (voxels): about FWD_SEG_TILE_MB of z-prefix per tile, a power of two in [16, 256]
     const double per_col = 8.0 * (double)pfx_stride_of(G);
-    int T = 32;
-    while (T < 256 && (double)(2 * T) * (2 * T) * per_col <= 32.0 * 1024 * 1024) T *= 2;
+    int T = 16;
+    while (T < 256 && (double)(2 * T) * (2 * T) * per_col <= FWD_SEG_TILE_MB * 1024.0 * 1024.0) T *= 2;
     const int ntx = (G.nx + T - 1) / T, nty = (G.ny + T - 1) / T;
     struct E {
         long long key;
