@@ -532,7 +532,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
                     help="single-thread oracle sample length (the all-core figure is one whole sub-iteration)")
+    ap.add_argument("--lib", default=None,
+                    help="A/B of a tuning variant of libctrecon.so (scripts/build_variants.py); not for results")
     args = ap.parse_args()
+    if args.lib:
+        from paper_1512_04564_b200 import ctrecon as C
+        C.LIB_PATH = os.path.abspath(args.lib)
     if args.warmup < 1:
         raise SystemExit("--warmup must be >= 1")
     if args.impl == "reference":

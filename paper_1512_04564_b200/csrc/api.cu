@@ -28,6 +28,17 @@ static std::atomic<int64_t> g_launches{0};
 
 namespace ctr {
 int64_t launches_add(int64_t n) { return g_launches.fetch_add(n) + n; }
+thread_local bool g_pdl = false;
+#ifndef CTR_PDL
+#define CTR_PDL 1   // programmatic dependent launch inside the solve's sub-iteration graph
+#endif
+
+// programmatic dependent launches for the kernels enqueued in this scope (kernels.cuh)
+struct PdlScope {
+    bool old;
+    explicit PdlScope(bool on) : old(g_pdl) { g_pdl = on; }
+    ~PdlScope() { g_pdl = old; }
+};
 }  // namespace ctr
 
 static ct_status fail(ct_status st, const char* fmt, ...) {
@@ -728,6 +739,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     int iter_out = 0;
     long long kcur = st->k;
     cudaGraphExec_t exec = nullptr;
+    const int kernels_per_subiter = (xt && fwd_nseg_of(g)) ? 4 : 3;   // + the segment reduce
     if (!dist && !kernel_ms && n_subiters > 0) {
         GraphKey key;
         key.ptrs = {(uintptr_t)ctl, (uintptr_t)st->x, (uintptr_t)xalt, (uintptr_t)y, (uintptr_t)w,
@@ -744,15 +756,20 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         } else {
             cudaStream_t cs = g->cap_stream;
             CT_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            enqueue_subiter(g, rp, ctl, st->x, xalt, xt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count, Mf,
-                            lo, hi, part, cs);
+            {
+                // the sub-iteration's kernels chained by programmatic dependent launch: each grid
+                // is scheduled during its predecessor's tail and waits for it (griddepcontrol)
+                PdlScope pdl(CTR_PDL != 0);
+                enqueue_subiter(g, rp, ctl, st->x, xalt, xt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count,
+                                Mf, lo, hi, part, cs);
+            }
             cudaGraph_t graph;
             cudaError_t e = cudaStreamEndCapture(cs, &graph);
             if (e != cudaSuccess) return fail(CT_E_CUDA, "graph capture: %s", cudaGetErrorString(e));
             e = cudaGraphInstantiate(&exec, graph, 0);
             cudaGraphDestroy(graph);
             if (e != cudaSuccess) return fail(CT_E_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
-            launches_add(-3);  // capture is not a launch; replays are counted below
+            launches_add(-kernels_per_subiter);  // capture is not a launch; replays are counted below
             const_cast<ct_geom*>(g)->graphs[key] = exec;
         }
     }
@@ -813,7 +830,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         cudaEvent_t* ev = kernel_ms ? &evs[(size_t)done * 5] : nullptr;
         if (exec) {
             CT_CUDA(cudaGraphLaunch(exec, s));
-            launches_add(3);
+            launches_add(kernels_per_subiter);
         } else if (!dist) {
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);

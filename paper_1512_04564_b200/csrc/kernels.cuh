@@ -1,10 +1,51 @@
 // kernels.cuh — host-side launcher declarations for libctrecon.so kernels.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <vector>
 
 #include "ct_internal.cuh"
 
 namespace ctr {
+
+// Programmatic dependent launch (PDL) for the kernels of a solver sub-iteration: while g_pdl is
+// set (the single-GPU sub-iteration graph's capture), launch_k launches with programmatic stream
+// serialization; every such kernel starts with pdl_enter(), which waits for its predecessor's
+// completion and memory (griddepcontrol.wait) before touching any data.  The dependent grid is
+// launched at the predecessor's exit (implicit trigger): c1 +2.2%, c2 +0.4% (launch latency).  An
+// early trigger at kernel entry (griddepcontrol.launch_dependents, CTR_PDL_TRIGGER=1) let waiting
+// blocks occupy the SMs during the predecessor's tail and was slower (c1 -26%, c3 -12%;
+// profiles/r2s/pdl_ab.log).  Without the launch attribute both instructions are no-ops.
+extern thread_local bool g_pdl;
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    if (!g_pdl) {
+        kern<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+#ifndef CTR_PDL_TRIGGER
+#define CTR_PDL_TRIGGER 0   // 1: early trigger at kernel entry (measured: c1 -26%, c3 -12%)
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if CTR_PDL_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 enum FwdMode { FWD_PLAIN = 0, FWD_RESID = 1, FWD_ONES_W = 2 };
 enum BackEpi { BK_WRITE = 0, BK_ACCUM = 1, BK_INIT = 2, BK_UPDATE = 3 };

@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(BK_BS * VS)
 k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
+    pdl_enter();
     __shared__ float red[VS][BK_Y][32];
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * BK_Y + threadIdx.y;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(BK_BS, BK_KZ <= 16 ? 7 : BK_KZ <= 24 ? BK_MINB
 k_back3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ proj, float scale, float* __restrict__ out, float* __restrict__ gbuf,
         float* __restrict__ htbuf) {
+    pdl_enter();
     constexpr int RM = BK_KZ <= 8 ? 14 : BK_KZ <= 16 ? BK_RMAX3 : BK_KZ <= 24 ? BK_RM24 : 44;
     __shared__ float2 csb[RM + 1][BK_BS];
     const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -369,18 +371,18 @@ static void back3_dispatch_kz(const DGeom& G, const float4* vtab, const Ctl* ctl
     dim3 grid((G.nx + 31) / 32, (G.ny + BK_Y - 1) / BK_Y, (G.nz + KZ - 1) / KZ);
     switch (epi) {
         case BK_WRITE:
-            if (lz) k_back3<ARC, BK_WRITE, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back3<ARC, BK_WRITE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            if (lz) launch_k(k_back3<ARC, BK_WRITE, true, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
+            else launch_k(k_back3<ARC, BK_WRITE, false, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         case BK_ACCUM:
-            if (lz) k_back3<ARC, BK_ACCUM, true, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
-            else k_back3<ARC, BK_ACCUM, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            if (lz) launch_k(k_back3<ARC, BK_ACCUM, true, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
+            else launch_k(k_back3<ARC, BK_ACCUM, false, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         case BK_INIT:
-            k_back3<ARC, BK_INIT, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            launch_k(k_back3<ARC, BK_INIT, false, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
         default:
-            k_back3<ARC, BK_UPDATE, false, KZ><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht);
+            launch_k(k_back3<ARC, BK_UPDATE, false, KZ>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht);
             break;
     }
 }
@@ -393,10 +395,10 @@ static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, V
     if ((long long)grid.x * grid.y < 148LL * 4) {
         dim3 block(32, BK_Y, 4);
         switch (epi) {
-            case BK_WRITE: k_back2<ARC, BK_WRITE, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            case BK_ACCUM: k_back2<ARC, BK_ACCUM, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            case BK_INIT: k_back2<ARC, BK_INIT, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            default: k_back2<ARC, BK_UPDATE, 4><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_WRITE: launch_k(k_back2<ARC, BK_WRITE, 4>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_ACCUM: launch_k(k_back2<ARC, BK_ACCUM, 4>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_INIT: launch_k(k_back2<ARC, BK_INIT, 4>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            default: launch_k(k_back2<ARC, BK_UPDATE, 4>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
         }
         return;
     }
@@ -404,19 +406,19 @@ static void back2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, V
     if ((long long)grid.x * grid.y < 148LL * 16) {
         dim3 block(32, BK_Y, 2);
         switch (epi) {
-            case BK_WRITE: k_back2<ARC, BK_WRITE, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            case BK_ACCUM: k_back2<ARC, BK_ACCUM, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            case BK_INIT: k_back2<ARC, BK_INIT, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-            default: k_back2<ARC, BK_UPDATE, 2><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_WRITE: launch_k(k_back2<ARC, BK_WRITE, 2>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_ACCUM: launch_k(k_back2<ARC, BK_ACCUM, 2>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            case BK_INIT: launch_k(k_back2<ARC, BK_INIT, 2>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+            default: launch_k(k_back2<ARC, BK_UPDATE, 2>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
         }
         return;
     }
     dim3 block(32, BK_Y, 1);
     switch (epi) {
-        case BK_WRITE: k_back2<ARC, BK_WRITE, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        case BK_ACCUM: k_back2<ARC, BK_ACCUM, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        case BK_INIT: k_back2<ARC, BK_INIT, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
-        default: k_back2<ARC, BK_UPDATE, 1><<<grid, block, 0, s>>>(G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_WRITE: launch_k(k_back2<ARC, BK_WRITE, 1>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_ACCUM: launch_k(k_back2<ARC, BK_ACCUM, 1>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        case BK_INIT: launch_k(k_back2<ARC, BK_INIT, 1>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
+        default: launch_k(k_back2<ARC, BK_UPDATE, 1>, grid, block, 0, s, G, vtab, ctl, v, proj, scale, out, g, ht); break;
     }
 }
 

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(32 * F2_WARPS)
 k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out) {
+    pdl_enter();
     constexpr bool ONES = (MODE == FWD_ONES_W);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const Views V = select_views(ctl, vsel);
@@ -279,6 +280,7 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
        const float* __restrict__ w, float* __restrict__ out, int pfx_stride, int slot_entries,
        const int2* __restrict__ sched, int seg_len, int part_views) {
+    pdl_enter();
     constexpr bool TMA = PFX && F3_TMA;
     constexpr int TD = F3_TMAD;
     extern __shared__ __align__(16) float2 fwd_ring[];   // TMA: [NW][TD][slot_entries]
@@ -707,8 +709,7 @@ static void fwd3_launch(const DGeom& G, dim3 grid, const float4* vtab, const Ctl
     const size_t smem = (size_t)NW * F3_TMAD * se * sizeof(float2);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_fwd3<ARC, MODE, RPL, PFX, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_fwd3<ARC, MODE, RPL, PFX, NW>
-        <<<grid, 32 * NW, smem, s>>>(G, vtab, ctl, v, xa, xb, y, w, out, ps, se, nullptr, 0, 0);
+    launch_k(k_fwd3<ARC, MODE, RPL, PFX, NW>, grid, 32 * NW, smem, s, G, vtab, ctl, v, xa, xb, y, w, out, ps, se, nullptr, 0, 0);
 }
 
 template <bool ARC, int MODE, bool PFX, int NW>
@@ -753,9 +754,9 @@ static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Vi
                           cudaStream_t s) {
     dim3 grid((G.ns + F2_CPW * F2_GPB - 1) / (F2_CPW * F2_GPB), max_count);
     const int bs = 32 * F2_WARPS;
-    if (mode == FWD_PLAIN) k_fwd2<ARC, FWD_PLAIN><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-    else if (mode == FWD_RESID) k_fwd2<ARC, FWD_RESID><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
-    else k_fwd2<ARC, FWD_ONES_W><<<grid, bs, 0, s>>>(G, vtab, ctl, v, xa, xb, y, w, out);
+    if (mode == FWD_PLAIN) launch_k(k_fwd2<ARC, FWD_PLAIN>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+    else if (mode == FWD_RESID) launch_k(k_fwd2<ARC, FWD_RESID>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+    else launch_k(k_fwd2<ARC, FWD_ONES_W>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
 }
 
 // r / L_z(s, t): the solver's residual buffer holds L_z W (A x - y) (L_z folded in for the
@@ -865,6 +866,7 @@ __global__ void __launch_bounds__(256) k_fwd3_reduce(DGeom G, const Ctl* __restr
                                                      const float* __restrict__ part, int nseg, int part_views,
                                                      const float* __restrict__ y, const float* __restrict__ w,
                                                      float* __restrict__ out) {
+    pdl_enter();
     const Views V = select_views(ctl, vsel);
     const long long per = (long long)G.nt * G.ns;
     const long long n = (long long)V.count * per, pstride = (long long)part_views * per;
@@ -891,7 +893,7 @@ template <bool ARC, int RPL, int NW>
 static void fwd3_seg_launch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, const float* pfx,
                             int ps, const int2* sched, int nsched, int seg_len, int max_count, float* part,
                             cudaStream_t s) {
-    k_fwd3<ARC, FWD_PLAIN, RPL, true, NW, true><<<nsched, 32 * NW, 0, s>>>(
+    launch_k(k_fwd3<ARC, FWD_PLAIN, RPL, true, NW, true>, nsched, 32 * NW, 0, s, 
         G, vtab, ctl, v, pfx, pfx, nullptr, nullptr, part, ps, 0, sched, seg_len, max_count);
 }
 
@@ -913,9 +915,9 @@ void launch_fwd_seg(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v,
     const long long n = (long long)max_count * G.nt * G.ns;
     const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
 #define CTR_RED(ARC)                                                                                               \
-    if (mode == FWD_PLAIN) k_fwd3_reduce<ARC, FWD_PLAIN><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out); \
-    else if (mode == FWD_RESID) k_fwd3_reduce<ARC, FWD_RESID><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out); \
-    else k_fwd3_reduce<ARC, FWD_ONES_W><<<blocks, 256, 0, s>>>(G, ctl, v, part, nseg, max_count, y, w, out);
+    if (mode == FWD_PLAIN) launch_k(k_fwd3_reduce<ARC, FWD_PLAIN>, blocks, 256, 0, s, G, ctl, v, part, nseg, max_count, y, w, out); \
+    else if (mode == FWD_RESID) launch_k(k_fwd3_reduce<ARC, FWD_RESID>, blocks, 256, 0, s, G, ctl, v, part, nseg, max_count, y, w, out); \
+    else launch_k(k_fwd3_reduce<ARC, FWD_ONES_W>, blocks, 256, 0, s, G, ctl, v, part, nseg, max_count, y, w, out);
     if (G.arc) {
         CTR_RED(true)
     } else {

@@ -186,6 +186,7 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 #endif
 template <int POT, int NDIRS, bool KAPPA, int MODE>
 __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp, const Ctl* __restrict__ ctl, UpdArgs A) {
+    pdl_enter();
     extern __shared__ float upd_sm[];  // pfx: xs[JPB][nz][33], tot[JPB][NZC][32]
     constexpr bool FULL = (MODE == UPD_FULL);
     const int lane = threadIdx.x, c = threadIdx.y, jj = threadIdx.z;
@@ -419,7 +420,7 @@ static void upd_launch(const DGeom& G, const RegParams& rp, const Ctl* ctl, UpdA
     if (u.smem > 48 * 1024)
         cudaFuncSetAttribute(k_update<POT, NDIRS, KAPPA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)u.smem);
-    k_update<POT, NDIRS, KAPPA, MODE><<<grid, block, u.smem, s>>>(G, rp, ctl, A);
+    launch_k(k_update<POT, NDIRS, KAPPA, MODE>, grid, block, u.smem, s, G, rp, ctl, A);
 }
 
 template <int MODE>
