@@ -336,15 +336,13 @@ static ct_status seg_sched(const ct_geom* g, int stride, int count, const SegSch
     return CT_OK;
 }
 
-// z-prefix forward of `max_count` views (from ctl, or v), segmented when fwd_nseg_of(g) > 0 (part:
-// the partial buffer, fwd_part_floats(g, max_count) floats; the schedule must exist already).
-static void fwd_pfx(const ct_geom* g, const Ctl* ctl, Views v, int sched_stride, int max_count, const float* xt,
+// z-prefix forward of `max_count` views (from ctl, or v), segmented when S != nullptr (S from
+// seg_sched, obtained before any graph capture; part: fwd_part_floats(g, max_count) floats).
+static void fwd_pfx(const ct_geom* g, const Ctl* ctl, Views v, const SegSched* S, int max_count, const float* xt,
                     const float* y, const float* w, float* out, int mode, float* part, cudaStream_t s) {
-    if (fwd_nseg_of(g) && part) {
-        const auto it = g->seg.find(std::make_pair(sched_stride, max_count));
-        const SegSched& S = it->second;
-        launch_fwd_seg(g->G, g->vtab, ctl, v, max_count, xt, y, w, out, mode, s, pfx_stride_of(g->G), S.d, S.n,
-                       S.seg_len, S.nseg, part);
+    if (S) {
+        launch_fwd_seg(g->G, g->vtab, ctl, v, max_count, xt, y, w, out, mode, s, pfx_stride_of(g->G), S->d, S->n,
+                       S->seg_len, S->nseg, part);
     } else {
         launch_fwd(g->G, g->vtab, ctl, v, max_count, xt, xt, y, w, out, mode, s, pfx_stride_of(g->G));
     }
@@ -420,7 +418,7 @@ extern "C" ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_vie
         const SegSched* S;
         st = seg_sched(g, v.stride, cnt, &S);
         if (st != CT_OK) return st;
-        fwd_pfx(g, nullptr, Views{v.start + c0 * v.stride, v.stride, cnt}, v.stride, cnt, pfx, nullptr, nullptr,
+        fwd_pfx(g, nullptr, Views{v.start + c0 * v.stride, v.stride, cnt}, S, cnt, pfx, nullptr, nullptr,
                 proj + (size_t)c0 * g->G.nt * g->G.ns, FWD_PLAIN, part, (cudaStream_t)s);
     }
     return check_async();
@@ -618,9 +616,9 @@ extern "C" double oslalm_rho(int64_t k, double alpha) {
 static void enqueue_subiter(const ct_geom* g, const RegParams& rp, Ctl* ctl, float* xa, float* xb, float* xt,
                             const float* y, const float* w, const float* dl, float* gb, float* ht,
                             const float* kappa, float* r, int max_count, float M, float lo, float hi,
-                            float* part, cudaStream_t s) {
+                            const SegSched* segs, float* part, cudaStream_t s) {
     launch_update(g->G, rp, ctl, xa, xb, dl, gb, ht, kappa, lo, hi, xt, s);
-    if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, (int)M, max_count, xt, y, w, r, FWD_RESID, part, s);
+    if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, segs, max_count, xt, y, w, r, FWD_RESID, part, s);
     else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, xa, xb, y, w, r, FWD_RESID, s);
     launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, r, M, BK_UPDATE, false, nullptr, gb, ht, s);   // + k advance
 }
@@ -668,9 +666,9 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
         return fail(CT_E_SHAPE, "subset projection block exceeds 2^31 elements (increase M)");
     const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
     const int sstride = world * M;   // view stride of a rank's subset (the segmented forward's schedule)
+    const SegSched* segs = nullptr;   // the segmented forward's schedule (nullptr: unsegmented)
     if (xt && fwd_nseg_of(g)) {
-        const SegSched* S;
-        ct_status e = seg_sched(g, sstride, max_count, &S);
+        ct_status e = seg_sched(g, sstride, max_count, &segs);
         if (e != CT_OK) return e;
     }
 
@@ -739,7 +737,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     int iter_out = 0;
     long long kcur = st->k;
     cudaGraphExec_t exec = nullptr;
-    const int kernels_per_subiter = (xt && fwd_nseg_of(g)) ? 4 : 3;   // + the segment reduce
+    const int kernels_per_subiter = segs ? 4 : 3;   // + the segment reduce
     if (!dist && !kernel_ms && n_subiters > 0) {
         GraphKey key;
         key.ptrs = {(uintptr_t)ctl, (uintptr_t)st->x, (uintptr_t)xalt, (uintptr_t)y, (uintptr_t)w,
@@ -761,7 +759,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                 // is scheduled during its predecessor's tail and waits for it (griddepcontrol)
                 PdlScope pdl(CTR_PDL != 0);
                 enqueue_subiter(g, rp, ctl, st->x, xalt, xt, y, w, d_l, st->g, st->htilde, kappa, rbuf, max_count,
-                                Mf, lo, hi, part, cs);
+                                Mf, lo, hi, segs, part, cs);
             }
             cudaGraph_t graph;
             cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -835,7 +833,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             if (ev) CT_CUDA(cudaEventRecord(ev[0], s));
             launch_update(g->G, rp, ctl, st->x, xalt, d_l, st->g, st->htilde, kappa, lo, hi, xt, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[1], s));
-            if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, sstride, max_count, xt, y, w, rbuf, FWD_RESID, part, s);
+            if (xt) fwd_pfx(g, ctl, Views{0, 1, 0}, segs, max_count, xt, y, w, rbuf, FWD_RESID, part, s);
             else launch_fwd(g->G, g->vtab, ctl, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rbuf, FWD_RESID, s);
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));
             launch_back(g->G, g->vtab, ctl, Views{0, 1, 0}, rbuf, Mf, BK_UPDATE, false, nullptr, st->g, st->htilde, s);
@@ -891,7 +889,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
             }
             for (int q = 0; q < nl; q++) {
                 float* rq = rbuf + q * rstride;
-                if (xt) fwd_pfx(g, ctl + q, Views{0, 1, 0}, sstride, max_count, xt, y, w, rq, FWD_RESID, part, s);
+                if (xt) fwd_pfx(g, ctl + q, Views{0, 1, 0}, segs, max_count, xt, y, w, rq, FWD_RESID, part, s);
                 else launch_fwd(G, g->vtab, ctl + q, Views{0, 1, 0}, max_count, st->x, xalt, y, w, rq, FWD_RESID, s);
             }
             if (ev) CT_CUDA(cudaEventRecord(ev[2], s));

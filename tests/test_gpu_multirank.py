@@ -136,3 +136,33 @@ def test_local_world_larger_than_planes_is_rejected(C):
         rec.close()
     finally:
         C.ct_dist_destroy(d)
+
+
+@pytest.mark.parametrize("kind,world,nseg", [("helical_mid", 2, 3), ("helical_mid", 4, 2)])
+def test_local_view_sharding_segmented_forward(C, kind, world, nseg):
+    """The emulated ranks with the segmented forward (ct_geom_set_fwd_segments, automatic at
+    c5): every rank's forward runs through its own schedule key (view stride world * M) and
+    the shared partial buffer; x, g, htilde against the oracle after 1, 3 and 2M sub-iterations."""
+    from paper_1512_04564_b200.recon import Recon
+    g = _geom(kind)
+    M = 3
+    pb = synthetic_problem(g, M=M)
+    prob = oracle_problem(pb)
+    trace = {}
+    alg.alg1(prob, pb["x0"], M, 1.999, 2, DL=pb["DL"], trace=trace)
+    d = C.ct_dist_create_local(world, 0)
+    try:
+        rec = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], dist=d, fwd_segments=nseg)
+        assert C.ct_geom_fwd_segments(rec.h) == nseg
+        rec.set_DL(pb["DL"])
+        done = 0
+        for k in (1, 3, 2 * M):
+            rec.run(k - done)
+            done = k
+            xo, go, ho = trace[k]
+            assert rel(host(rec.x), xo) <= 1e-4, (k, rel(host(rec.x), xo))
+            assert rel(host(rec.g), go) <= 1e-3, (k, rel(host(rec.g), go))
+            assert rel(host(rec.htilde), pb["DL"] * xo - ho) <= 1e-3, k
+        rec.close()
+    finally:
+        C.ct_dist_destroy(d)
