@@ -234,9 +234,6 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
                  : "memory");
 }
 
-#ifndef F3_HITFENCE
-#define F3_HITFENCE 0  // experiment: compiler barrier after each hit of the hit loop
-#endif
 #ifndef F3_CREDIT2
 #define F3_CREDIT2 0   // a hit's credits to the 4 detector columns as packed FP32 pairs (FFMA2)
 #endif
@@ -632,9 +629,6 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
                         acc[3][r] = fmaf(L4.w, Rs[r], acc[3][r]);
 #endif
                     }
-#if F3_HITFENCE
-                    asm volatile("" ::: "memory");   // experiment: keep hits from being interleaved
-#endif
                 }
                 if (TMA) tcnt += n;
                 __syncwarp();
