@@ -234,6 +234,9 @@ __device__ __forceinline__ void bulk_copy(unsigned dst, const void* src, unsigne
                  : "memory");
 }
 
+#ifndef F3_VIEWCULL
+#define F3_VIEWCULL 1  // skip the walk of views whose cone misses the volume (thin z-slabs)
+#endif
 #ifndef F3_CREDIT2
 #define F3_CREDIT2 0   // a hit's credits to the 4 detector columns as packed FP32 pairs (FFMA2)
 #endif
@@ -364,7 +367,17 @@ k_fwd3(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
     }
 #endif
 
-    if (s0 < G.ns) {  // warp-uniform
+    // view cull (block-uniform): the voxel columns span detector rows [(zbot - z_s) m + t_c0p,
+    // (ztop - z_s) m + t_c0p] for a magnification m (rows per mm) in [mlo, mhi]; a view whose cone
+    // misses the volume (helical views beyond a thin z-slab, the ends of a long helix) projects to 0
+    // and skips the walk (the epilogue still writes its outputs)
+    bool reach = true;
+    if (F3_VIEWCULL) {
+        const float mlo = G.dsd / (G.dso + G.rxy) * G.inv_dt, mhi = G.dsd / (G.dso - G.rxy) * G.inv_dt;
+        const float za = G.zbot - zs, zb = G.ztop - zs;
+        reach = fminf(za * mlo, za * mhi) + G.t_c0p < (float)G.nt + 1.f && fmaxf(zb * mlo, zb * mhi) + G.t_c0p > -1.f;
+    }
+    if (s0 < G.ns && reach) {  // warp-uniform
         const int s3 = min(s0 + F3_CPW - 1, G.ns - 1);
         const float tl = ((float)s0 - 0.5f - G.s_c0) * G.delta;
         const float tr = ((float)s3 + 0.5f - G.s_c0) * G.delta;
