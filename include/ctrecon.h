@@ -186,17 +186,20 @@ ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_views v, float
  * the wedge of every detector-column block is walked in nseg slab segments,
  * scheduled so that resident blocks share one xy tile of the z-prefix in L2,
  * and the segments' raw row sums are added in segment order (deterministic)
- * before the epilogue.  For volumes whose z-prefix array exceeds L2 (c5),
- * where every view otherwise re-streams its band of it from HBM.
- * nseg: -1 automatic (16 when the z-prefix array exceeds 512 MB, else off,
- * the default), 0 or 1 off, 2..64 forced.  Applies to ct_forward_zprefix and
- * oslalm_relaxed_solve / oslalm_profile of this geometry; it changes
- * ct_zprefix_size and oslalm_workspace_size (query them after setting it).
- * Frees the geometry's cached solve graphs; call it while no work of this
- * geometry is in flight.  ct_geom_fwd_segments returns the effective count
- * (0 = unsegmented).  Errors: CT_E_CONFIG (NULL, nseg outside [-1, 64]). */
+ * before the epilogue.
+ * nseg: -1 automatic (the default): 16 when the z-prefix array exceeds 512 MB
+ * (c5, where every view otherwise re-streams its band of it from HBM); for
+ * 3-D volumes of at least 256 x 256 columns as many (<= 8) as keep the
+ * partial sums of one launch within 96 MB (c4: 3, c3: 8); else off.  0 or 1:
+ * off; 2..64: forced.  Applies to ct_forward_zprefix (launches of <= 128
+ * views) and oslalm_relaxed_solve / oslalm_profile (one subset per launch) of
+ * this geometry; it changes ct_zprefix_size and oslalm_workspace_size (query
+ * them after setting it).  Frees the geometry's cached solve graphs; call it
+ * while no work of this geometry is in flight.  ct_geom_fwd_segments returns
+ * the count used for a launch of `views` views (0 = unsegmented).
+ * Errors: CT_E_CONFIG (NULL, nseg outside [-1, 64]). */
 ct_status ct_geom_set_fwd_segments(ct_geom* g, int nseg);
-ct_status ct_geom_fwd_segments(const ct_geom* g, int* nseg);
+ct_status ct_geom_fwd_segments(const ct_geom* g, int views, int* nseg);
 
 /* x_out (=|+=) scale * A' proj on views v.
  * proj: float[v.count][nt][ns]; accumulate != 0 adds into x_out. */

@@ -92,21 +92,29 @@ struct ct_geom {
     cudaStream_t cap_stream;  // private stream for graph capture
     std::mutex mu;            // guards the graph and schedule caches (the geometry itself is immutable)
     std::map<GraphKey, cudaGraphExec_t> graphs;
-    std::map<std::pair<int, int>, SegSched> seg;
+    std::map<std::tuple<int, int, int>, SegSched> seg;   // (view stride, views, segments)
 };
 
-// Segments of the z-prefix forward: automatic = 16 when the z-prefix array exceeds 512 MB (c5:
-// 2.2 GB; every view would otherwise re-stream its band of it from HBM), else none.
-static int fwd_nseg_of(const ct_geom* g) {
+// Segments of the z-prefix forward of `views` views per launch (0 = unsegmented).
+// Automatic: 16 when the z-prefix array exceeds 512 MB (c5: 2.2 GB; every view would otherwise
+// re-stream its band of it from HBM); for volumes of at least 256 x 256 columns, as many as keep
+// the partial sums within 96 MB (at most 8; measured optimum c4: 3, c3: 8, profiles/r2s/
+// nseg_sweep.log: the tile-ordered walk's L2 hit rate against the partials' traffic); otherwise
+// none (small volumes, 2-D).
+static int fwd_nseg_of(const ct_geom* g, long long views) {
     if (g->G.dim != 3) return 0;
     if (g->fwd_nseg >= 0) return g->fwd_nseg >= 2 ? g->fwd_nseg : 0;
     const double pfx = 8.0 * (double)g->G.nxy * (double)pfx_stride_of(g->G);
-    return pfx > 512.0 * 1024.0 * 1024.0 ? 16 : 0;
+    if (pfx > 512.0 * 1024.0 * 1024.0) return 16;
+    if (g->G.nxy < 256LL * 256LL || views < 1) return 0;
+    const double per = 4.0 * (double)views * g->G.nt * g->G.ns;
+    const int n = (int)std::min(8.0, std::floor(96.0 * 1024.0 * 1024.0 / per));
+    return n >= 2 ? n : 0;
 }
 
 // floats of the segmented forward's partial buffer for up to `count` views (0 = unsegmented)
 static size_t fwd_part_floats(const ct_geom* g, long long count) {
-    const int ns = fwd_nseg_of(g);
+    const int ns = fwd_nseg_of(g, count);
     return ns ? (size_t)ns * (size_t)count * g->G.nt * g->G.ns : 0;
 }
 
@@ -317,13 +325,12 @@ static Views to_views(ct_views v) { return Views{v.start, v.stride, v.count}; }
 // The segmented forward's schedule for views of stride `stride` (angles of start 0; the order is
 // a locality heuristic only), built and uploaded on first use -- never inside a graph capture
 // (solve_impl and ct_forward_zprefix build it before enqueueing).
-static ct_status seg_sched(const ct_geom* g, int stride, int count, const SegSched** out) {
+static ct_status seg_sched(const ct_geom* g, int stride, int count, int nseg, const SegSched** out) {
     ct_geom* gm = const_cast<ct_geom*>(g);
     std::lock_guard<std::mutex> lk(gm->mu);
-    const auto key = std::make_pair(stride, count);
+    const auto key = std::make_tuple(stride, count, nseg);
     auto it = gm->seg.find(key);
-    if (it == gm->seg.end() || it->second.nseg == 0) {
-        const int nseg = fwd_nseg_of(g);
+    if (it == gm->seg.end()) {
         SegSched S;
         std::vector<int2> h = fwd_seg_schedule(g->G, g->htab, Views{0, stride, count}, count, nseg, &S.seg_len);
         S.n = (int)h.size();
@@ -362,9 +369,9 @@ extern "C" ct_status ct_geom_set_fwd_segments(ct_geom* g, int nseg) {
     return CT_OK;
 }
 
-extern "C" ct_status ct_geom_fwd_segments(const ct_geom* g, int* nseg) {
+extern "C" ct_status ct_geom_fwd_segments(const ct_geom* g, int views, int* nseg) {
     if (!g || !nseg) return fail(CT_E_CONFIG, "ct_geom_fwd_segments: NULL argument");
-    *nseg = fwd_nseg_of(g);
+    *nseg = fwd_nseg_of(g, views);
     return CT_OK;
 }
 
@@ -406,7 +413,9 @@ extern "C" ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_vie
     DeviceGuard guard(g->device);
     float* pfx = (float*)workspace;
     launch_zprefix(g->G, x, pfx, (cudaStream_t)s);
-    if (!fwd_nseg_of(g)) {
+    // one segment count for every chunk of this call (the partial buffer is sized for it)
+    const int nseg = fwd_nseg_of(g, std::min(kZpfxChunk, g->d.na));
+    if (!nseg) {
         launch_fwd(g->G, g->vtab, nullptr, to_views(v), v.count, pfx, pfx, nullptr, nullptr, proj, FWD_PLAIN,
                    (cudaStream_t)s, pfx_stride_of(g->G));
         return check_async();
@@ -416,7 +425,7 @@ extern "C" ct_status ct_forward_zprefix(const ct_geom* g, const float* x, ct_vie
     for (int c0 = 0; c0 < v.count; c0 += kZpfxChunk) {
         const int cnt = std::min(kZpfxChunk, v.count - c0);
         const SegSched* S;
-        st = seg_sched(g, v.stride, cnt, &S);
+        st = seg_sched(g, v.stride, cnt, nseg, &S);
         if (st != CT_OK) return st;
         fwd_pfx(g, nullptr, Views{v.start + c0 * v.stride, v.stride, cnt}, S, cnt, pfx, nullptr, nullptr,
                 proj + (size_t)c0 * g->G.nt * g->G.ns, FWD_PLAIN, part, (cudaStream_t)s);
@@ -667,8 +676,9 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
     const float lo = (float)p->box_lo, hi = std::isinf(p->box_hi) ? 3.0e38f : (float)p->box_hi;
     const int sstride = world * M;   // view stride of a rank's subset (the segmented forward's schedule)
     const SegSched* segs = nullptr;   // the segmented forward's schedule (nullptr: unsegmented)
-    if (xt && fwd_nseg_of(g)) {
-        ct_status e = seg_sched(g, sstride, max_count, &segs);
+    const int nseg = xt ? fwd_nseg_of(g, max_count) : 0;
+    if (nseg) {
+        ct_status e = seg_sched(g, sstride, max_count, nseg, &segs);
         if (e != CT_OK) return e;
     }
 
@@ -745,7 +755,7 @@ static ct_status solve_impl(const ct_geom* g, const float* y, const float* w, co
                     (uintptr_t)xt};
         key.vals = {(double)M, p->alpha, (double)p->rho_mode, p->rho_fixed, (double)lo, (double)hi, (double)p->variant,
                     (double)rp.potential, (double)rp.delta, (double)rp.n_dirs, (double)rp.maxcurv, (double)rp.q,
-                    (double)fwd_nseg_of(g)};
+                    (double)nseg};
         for (int i = 0; i < 13; i++) key.vals.push_back(rp.beta[i]);
         std::lock_guard<std::mutex> lk(const_cast<ct_geom*>(g)->mu);
         auto it = g->graphs.find(key);

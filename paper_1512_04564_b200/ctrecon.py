@@ -92,7 +92,7 @@ def load():
     L.ct_zprefix_size.argtypes = [vp, P(ctypes.c_size_t)]
     L.ct_forward_zprefix.argtypes = [vp, vp, ct_views, vp, vp, ctypes.c_size_t, vp]
     L.ct_geom_set_fwd_segments.argtypes = [vp, ctypes.c_int]
-    L.ct_geom_fwd_segments.argtypes = [vp, P(ctypes.c_int)]
+    L.ct_geom_fwd_segments.argtypes = [vp, ctypes.c_int, P(ctypes.c_int)]
     L.oslalm_residual.argtypes = [vp, P(oslalm_params), vp, ctypes.c_int64, vp, ctypes.c_size_t, vp, vp]
     L.ct_sqs_diag.argtypes = [vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.ct_reg_grad.argtypes = [vp, P(ct_reg_desc), vp, vp, vp, vp, vp]
@@ -218,9 +218,10 @@ def ct_geom_set_fwd_segments(geom, nseg):
     _check(load().ct_geom_set_fwd_segments(geom, int(nseg)))
 
 
-def ct_geom_fwd_segments(geom):
+def ct_geom_fwd_segments(geom, views=128):
+    """Segments the z-prefix forward uses for a launch of `views` views (0 = unsegmented)."""
     n = ctypes.c_int()
-    _check(load().ct_geom_fwd_segments(geom, ctypes.byref(n)))
+    _check(load().ct_geom_fwd_segments(geom, int(views), ctypes.byref(n)))
     return n.value
 
 

@@ -36,4 +36,5 @@ rec.run(M)
 for r in range(reps):
     kms = C.oslalm_profile(rec.h, rec.y, rec.w, rec.reg, rec.kappa, rec.dl, rec.params, rec.state, M, rec.ws)
     print("lib=%s nseg=%d update %.4f fwd %.4f back %.4f ms/subiter" % (
-        os.path.basename(C.LIB_PATH), C.ct_geom_fwd_segments(rec.h), kms[0] / M, kms[1] / M, kms[2] / M))
+        os.path.basename(C.LIB_PATH), C.ct_geom_fwd_segments(rec.h, (cfg["geom"]["na"] + M - 1) // M),
+        kms[0] / M, kms[1] / M, kms[2] / M))

@@ -149,13 +149,13 @@ def test_segmented_forward_parity(C, kind, nseg):
     x = rng.random(P.vol_shape(g))
     h = C.ct_geom_create(C.geom_desc(g))
     try:
-        assert C.ct_geom_fwd_segments(h) == 0      # mid-size volumes: automatic = off
+        assert C.ct_geom_fwd_segments(h, na) == 0      # mid-size volumes (< 256 x 256 columns): automatic = off
         xd = dev(x)
         ws0 = torch.empty(C.ct_zprefix_size(h), dtype=torch.uint8, device="cuda")
         p0 = torch.empty(P.proj_shape(g, na), dtype=torch.float32, device="cuda")
         C.ct_forward_zprefix(h, xd, C.views(0, 1, na), p0, ws0)
         C.ct_geom_set_fwd_segments(h, nseg)
-        assert C.ct_geom_fwd_segments(h) == nseg
+        assert C.ct_geom_fwd_segments(h, na) == nseg
         ws = torch.empty(C.ct_zprefix_size(h), dtype=torch.uint8, device="cuda")
         assert ws.numel() > ws0.numel()
         ps = torch.empty_like(p0)
@@ -171,7 +171,7 @@ def test_segmented_forward_parity(C, kind, nseg):
         C.ct_forward_zprefix(h, xd, C.views(*vv), pv, ws)
         assert rel(host(pv), P.forward(g, x, vv)) <= 1e-4
         C.ct_geom_set_fwd_segments(h, -1)
-        assert C.ct_geom_fwd_segments(h) == 0
+        assert C.ct_geom_fwd_segments(h, na) == 0
     finally:
         C.ct_geom_destroy(h)
 
@@ -190,7 +190,7 @@ def test_segmented_solve_trace(C, kind, nseg):
     trace = {}
     alg.alg1(prob, pb["x0"], M, 1.999, 3, DL=DL, trace=trace)
     rec = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], fwd_segments=nseg)
-    assert C.ct_geom_fwd_segments(rec.h) == nseg
+    assert C.ct_geom_fwd_segments(rec.h, 200) == nseg
     rec.set_DL(DL)
     done = 0
     na = g["na"]
@@ -211,3 +211,23 @@ def test_segmented_solve_trace(C, kind, nseg):
         err = np.linalg.norm(host(r) - ro) / np.linalg.norm(wm * ax)
         assert err <= 1e-4, (k, err)
     rec.close()
+
+
+def test_automatic_segments_of_the_baseline_configs(C):
+    """The library's automatic segment count for one subset of each BASELINE 3-D config
+    (c5 16 for its 2.2 GB z-prefix, c4 3 and c3 8 from the 96 MB budget of partial
+    sums) and off for the 2-D configs; forcing and resetting it."""
+    from synth.configs import get_config
+    want = {"c1": 0, "c2": 0, "c3": 8, "c4": 3, "c5": 16}
+    for name, n in want.items():
+        cfg = get_config(name)
+        g, M = cfg["geom"], cfg["solver"]["M"]
+        h = C.ct_geom_create(C.geom_desc(g))
+        try:
+            assert C.ct_geom_fwd_segments(h, (g["na"] + M - 1) // M) == n, name
+            C.ct_geom_set_fwd_segments(h, 0)
+            assert C.ct_geom_fwd_segments(h, (g["na"] + M - 1) // M) == 0
+            C.ct_geom_set_fwd_segments(h, -1)
+            assert C.ct_geom_fwd_segments(h, (g["na"] + M - 1) // M) == n
+        finally:
+            C.ct_geom_destroy(h)

@@ -153,7 +153,7 @@ def test_local_view_sharding_segmented_forward(C, kind, world, nseg):
     d = C.ct_dist_create_local(world, 0)
     try:
         rec = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"], dist=d, fwd_segments=nseg)
-        assert C.ct_geom_fwd_segments(rec.h) == nseg
+        assert C.ct_geom_fwd_segments(rec.h, 200) == nseg
         rec.set_DL(pb["DL"])
         done = 0
         for k in (1, 3, 2 * M):
