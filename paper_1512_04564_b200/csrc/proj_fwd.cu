@@ -804,7 +804,7 @@ void launch_fwd(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int
 // Segmented z-prefix forward (SEG above).  The segment length is a multiple of the 32-slab pass
 // so that segments split no pass; the schedule is built on the host from the view table.
 #ifndef FWD_SEG_TILE_MB
-#define FWD_SEG_TILE_MB 32   // z-prefix bytes per schedule tile (c5: 64 x 64 columns)
+#define FWD_SEG_TILE_MB 40   // z-prefix MB per schedule tile (c5: 128^2, c4: 128^2, c3: 256^2 columns; profiles/r2s/tile_ab.log)
 #endif
 int fwd_seg_len(const DGeom& G, int nseg) {
     const int na = std::max(G.nx, G.ny);
