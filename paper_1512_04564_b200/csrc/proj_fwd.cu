@@ -163,6 +163,154 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 }
 
 // ---------------------------------------------------------------------------
+// 2-D forward projection, block-wide cell groups (k_fwd2b, the default; F2B = 0 selects k_fwd2
+// above).  A block of F2B_WARPS warps owns CPB = 16 or 32 adjacent detector cells of one view and
+// walks the union of their fan wedges; the warps take interleaved slab passes (F2B_SUB lanes per
+// slab split its candidate pixels).  Each candidate pixel's footprint is evaluated once for the
+// whole block (k_fwd2 evaluated it once per 8-cell warp group, ~1.25 times per pixel-view at c2)
+// and F1 only for the cells under it (nc + 1 antiderivative evaluations instead of 9); the credits
+// L_xy F1 x go to the lane's own row of a shared-memory tile [warp][lane][CPB + 1] (no atomics),
+// which is summed over lanes and warps in a fixed order at the end (deterministic).
+#ifndef F2B
+#define F2B 1
+#endif
+#ifndef F2B_CPB
+#define F2B_CPB 0      // cells per block: 0 = chosen per launch (32 / 16 / 8), else forced
+#endif
+#ifndef F2B_MINBPS
+#define F2B_MINBPS 4   // the widest group that still gives this many blocks per SM
+#endif
+constexpr int F2B_WARPS = 4;
+constexpr int F2B_SUB = 8;                 // lanes per slab
+constexpr int F2B_SPP = 32 / F2B_SUB;      // slabs per warp pass
+
+template <bool ARC, int MODE, int CPB>
+__global__ void __launch_bounds__(32 * F2B_WARPS)
+k_fwd2b(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
+        const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
+        const float* __restrict__ w, float* __restrict__ out) {
+    pdl_enter();
+    constexpr bool ONES = (MODE == FWD_ONES_W);
+    __shared__ float rows[F2B_WARPS * 32 * (CPB + 1)];
+    __shared__ float wsum[F2B_WARPS][CPB];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float* __restrict__ row = rows + (wid * 32 + lane) * (CPB + 1);
+#pragma unroll
+    for (int c = 0; c < CPB; c++) row[c] = 0.f;
+    const Views V = select_views(ctl, vsel);
+    const int vi = blockIdx.y;
+    if (vi >= V.count) return;   // block-uniform
+    const int v = V.start + vi * V.stride;
+    const int s0 = blockIdx.x * CPB;
+    const float* __restrict__ x = xa;
+    if (ctl) x = (((ctl->k - ctl->k_base) & 1) != 0) ? xa : xb;
+    const float4 vw = __ldg(&vtab[v]);
+    const float cb = vw.x, sb = vw.y;
+    const float Sx = G.dso * cb, Sy = G.dso * sb;
+    const int slast = min(s0 + CPB - 1, G.ns - 1);
+    const float tl = ((float)s0 - 0.5f - G.s_c0) * G.delta;
+    const float tr = ((float)slast + 0.5f - G.s_c0) * G.delta;
+    const float tm = (0.5f * (float)(s0 + slast) - G.s_c0) * G.delta;
+    float cal, cul, car, cur_, cam, cum;
+    if (ARC) {
+        sincosf(tl, &cul, &cal);
+        sincosf(tr, &cur_, &car);
+        sincosf(tm, &cum, &cam);
+    } else {
+        cal = car = cam = G.dsd;
+        cul = tl; cur_ = tr; cum = tm;
+    }
+    const float dlx = -cal * cb - cul * sb, dly = -cal * sb + cul * cb;
+    const float drx = -car * cb - cur_ * sb, dry = -car * sb + cur_ * cb;
+    const float dmx = -cam * cb - cum * sb, dmy = -cam * sb + cum * cb;
+    const float nlx = -cal * sb + cul * cb, nly = cal * cb + cul * sb;
+    const float nrx = car * sb - cur_ * cb, nry = -car * cb - cur_ * sb;
+    const float hx = 0.5f * G.dx, hy = 0.5f * G.dy;
+    const float suppl = fabsf(nlx) * hx + fabsf(nly) * hy;
+    const float suppr = fabsf(nrx) * hx + fabsf(nry) * hy;
+    const float tol_l = 1e-4f * suppl, tol_r = 1e-4f * suppr;
+    const bool xstep = fabsf(dmx) >= fabsf(dmy);
+    const int na_ = xstep ? G.nx : G.ny, no_ = xstep ? G.ny : G.nx;
+    const float a0 = xstep ? G.x0 : G.y0, da = xstep ? G.dx : G.dy, ha = xstep ? hx : hy;
+    const float o0 = xstep ? G.y0 : G.x0, dob = xstep ? G.dy : G.dx;
+    const float Sa = xstep ? Sx : Sy, So = xstep ? Sy : Sx;
+    const float kl = xstep ? dly / dlx : dlx / dly;
+    const float kr = xstep ? dry / drx : drx / dry;
+    const float sgn = (xstep ? dlx : dly) > 0.f ? 1.f : -1.f;
+    const float inv_do = 1.f / dob;
+    __syncwarp();
+
+    for (int sl0 = wid * F2B_SPP; sl0 < na_; sl0 += F2B_SPP * F2B_WARPS) {
+        const int sl = sl0 + lane / F2B_SUB, sub = lane % F2B_SUB;
+        int lo = 0, hi = -1;
+        if (sl < na_) {
+            const float ac = fmaf((float)sl, da, a0);
+            const float pa = ac - ha - Sa, pb = ac + ha - Sa;
+            if (pa * sgn > 0.f && pb * sgn > 0.f) {
+                const float y1 = fmaf(pa, kl, So), y2 = fmaf(pb, kl, So);
+                const float y3 = fmaf(pa, kr, So), y4 = fmaf(pb, kr, So);
+                const float f0 = (fminf(fminf(y1, y2), fminf(y3, y4)) - o0) * inv_do + 0.5f;
+                const float f1 = (fmaxf(fmaxf(y1, y2), fmaxf(y3, y4)) - o0) * inv_do + 0.5f;
+                if (f1 >= -1.f && f0 <= (float)no_ + 1.f) {
+                    lo = max((int)floorf(f0 - 1e-3f), 0);
+                    hi = min((int)floorf(f1 + 1e-3f), no_ - 1);
+                }
+            }
+        }
+        const int npass = __reduce_max_sync(0xffffffffu, (hi - lo + F2B_SUB) / F2B_SUB);
+        for (int p = 0; p < npass; p++) {
+            const int o = lo + sub + F2B_SUB * p;
+            if (o > hi) continue;
+            const int i = xstep ? sl : o, j = xstep ? o : sl;
+            const float cx = fmaf((float)i, G.dx, G.x0) - Sx;
+            const float cy = fmaf((float)j, G.dy, G.y0) - Sy;
+            if (fmaf(nlx, cx, nly * cy) + suppl < -tol_l || fmaf(nrx, cx, nry * cy) + suppr < -tol_r) continue;
+            Footprint f;
+            ct_footprint<ARC>(G, cb, sb, 0.f, i, j, f);
+            // cells under the footprint within the block's cells (the back-projector's range)
+            const int slo = max((int)floorf(f.sfc + f.u0 + 0.5f), s0);
+            const int shi = min((int)floorf(f.sfc + f.u3 + 0.5f), slast);
+            if (slo > shi) continue;
+            const float Lx = f.lxy * (ONES ? 1.f : __ldg(&x[(size_t)j * G.nx + i]));
+            float T0 = trap_T(f, ((float)slo - 0.5f) - f.sfc);
+            for (int sc = slo; sc <= shi; sc++) {
+                const float T1 = trap_T(f, ((float)sc + 0.5f) - f.sfc);
+                CTR_CHECK(sc - s0 >= 0 && sc - s0 < CPB, "fwd2b cell");
+                row[sc - s0] = fmaf(Lx, T1 - T0, row[sc - s0]);
+                T0 = T1;
+            }
+        }
+    }
+    // cell c: the 32 lane rows of each warp in lane order, then the warps in order
+    __syncwarp();
+    for (int c = lane; c < CPB; c += 32) {
+        float q = 0.f;
+        const float* __restrict__ col = rows + wid * 32 * (CPB + 1) + c;
+#pragma unroll 8
+        for (int l = 0; l < 32; l++) q += col[l * (CPB + 1)];
+        wsum[wid][c] = q;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < CPB; c += 32 * F2B_WARPS) {
+        const int sc = s0 + c;
+        float q = 0.f;
+#pragma unroll
+        for (int pw = 0; pw < F2B_WARPS; pw++) q += wsum[pw][c];
+        if (sc < G.ns) {
+            const size_t o = (size_t)vi * G.ns + sc;
+            if (MODE == FWD_PLAIN) {
+                out[o] = q;
+            } else {
+                const size_t a = (size_t)v * G.ns + sc;
+                const float wv = w ? __ldg(&w[a]) : 1.f;
+                if (MODE == FWD_RESID) out[o] = wv * (q - __ldg(&y[a]));
+                else out[o] = wv * q;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // 3-D forward projection.  A warp owns F3_CPW = 4 adjacent detector columns
 // s0..s0+3 of one view (the union of their fan wedges); lane l owns the RPL
 // consecutive detector rows t = RPL*l + r of all four columns.  The warp walks
@@ -759,6 +907,37 @@ template <bool ARC>
 static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Views v, int max_count,
                           const float* xa, const float* xb, const float* y, const float* w, float* out, int mode,
                           cudaStream_t s) {
+    if (F2B) {
+        // the widest cell group (32, 16, 8) that still gives >= 4 blocks per SM (c2: 32, c1: 16;
+        // measured, profiles/r2s/fwd2b_ab.log: wider groups evaluate each footprint fewer times)
+        const long long need = 148LL * F2B_MINBPS;
+        int cpb = F2B_CPB;
+        if (cpb == 0) cpb = (long long)((G.ns + 31) / 32) * max_count >= need ? 32
+                            : (long long)((G.ns + 15) / 16) * max_count >= need ? 16 : 8;
+        const int bs = 32 * F2B_WARPS;
+        if (cpb == 64) {
+            dim3 grid((G.ns + 63) / 64, max_count);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+        } else if (cpb == 8) {
+            dim3 grid((G.ns + 7) / 8, max_count);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+        } else if (cpb == 16) {
+            dim3 grid((G.ns + 15) / 16, max_count);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+        } else {
+            dim3 grid((G.ns + 31) / 32, max_count);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+        }
+        return;
+    }
     dim3 grid((G.ns + F2_CPW * F2_GPB - 1) / (F2_CPW * F2_GPB), max_count);
     const int bs = 32 * F2_WARPS;
     if (mode == FWD_PLAIN) launch_k(k_fwd2<ARC, FWD_PLAIN>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
