@@ -180,11 +180,14 @@ k_fwd2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Vi
 #ifndef F2B_MINBPS
 #define F2B_MINBPS 4   // the widest group that still gives this many blocks per SM
 #endif
-constexpr int F2B_WARPS = 4;
-constexpr int F2B_SUB = 8;                 // lanes per slab
+#ifndef F2B_LPS
+#define F2B_LPS 2      // lanes per slab (measured c2: 2 > 4 > 8 > 16, profiles/r2s/fwd2b_ab.log)
+#endif
+constexpr int F2B_SUB = F2B_LPS;           // lanes per slab
 constexpr int F2B_SPP = 32 / F2B_SUB;      // slabs per warp pass
 
-template <bool ARC, int MODE, int CPB>
+// F2B_WARPS warps per block: 8 for 32-cell groups (c2), 4 for 16 / 8 (c1) -- measured
+template <bool ARC, int MODE, int CPB, int F2B_WARPS>
 __global__ void __launch_bounds__(32 * F2B_WARPS)
 k_fwd2b(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, Views vsel,
         const float* __restrict__ xa, const float* __restrict__ xb, const float* __restrict__ y,
@@ -914,27 +917,21 @@ static void fwd2_dispatch(const DGeom& G, const float4* vtab, const Ctl* ctl, Vi
         int cpb = F2B_CPB;
         if (cpb == 0) cpb = (long long)((G.ns + 31) / 32) * max_count >= need ? 32
                             : (long long)((G.ns + 15) / 16) * max_count >= need ? 16 : 8;
-        const int bs = 32 * F2B_WARPS;
-        if (cpb == 64) {
-            dim3 grid((G.ns + 63) / 64, max_count);
-            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 64>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-        } else if (cpb == 8) {
+        if (cpb == 8) {
             dim3 grid((G.ns + 7) / 8, max_count);
-            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 8>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 8, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 8, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 8, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
         } else if (cpb == 16) {
             dim3 grid((G.ns + 15) / 16, max_count);
-            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 16>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 16, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 16, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 16, 4>, grid, 128, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
         } else {
             dim3 grid((G.ns + 31) / 32, max_count);
-            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
-            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 32>, grid, bs, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            if (mode == FWD_PLAIN) launch_k(k_fwd2b<ARC, FWD_PLAIN, 32, 8>, grid, 256, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else if (mode == FWD_RESID) launch_k(k_fwd2b<ARC, FWD_RESID, 32, 8>, grid, 256, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
+            else launch_k(k_fwd2b<ARC, FWD_ONES_W, 32, 8>, grid, 256, 0, s, G, vtab, ctl, v, xa, xb, y, w, out);
         }
         return;
     }
