@@ -13,6 +13,6 @@ for c in c1 c2 c3 c5; do python bench.py --config $c --steps 5 --warmup 3 --no-c
 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/plain_$tag.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$tag.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_fwd3|k_back3|k_update" -s 12 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_fwd3|k_back3|k_update" -s 12 -c 4 \
     -o gpurun_out/prof_$tag python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$tag.log 2>&1
 echo done

@@ -117,9 +117,11 @@ def main():
         key = "forward" if n.startswith(("k_fwd3", "k_fwd2")) else "back" if n.startswith("k_back") else \
             "update" if n.startswith("k_update") else None
         if key:
-            traffic[key] = (rd, wr)
+            # one launch per kernel: the segmented forward's walk and its reduce add up
+            prd, pwr = traffic.get(key, (0.0, 0.0))
+            traffic[key] = (prd + rd, pwr + wr)
             try:
-                inst[key] = float(d["smsp__inst_executed.sum"].replace(",", ""))
+                inst[key] = inst.get(key, 0.0) + float(d["smsp__inst_executed.sum"].replace(",", ""))
             except Exception:
                 pass
     units = dict(zip(list(csv.reader(io.StringIO(subprocess.run(
