@@ -522,6 +522,7 @@ static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp)
     if (r->potential == CT_POT_QGGMRF && !(r->q >= 1.0 && r->q <= 2.0))
         return fail(CT_E_CONFIG, "q-GGMRF needs 1 <= q <= 2 (got %g)", r->q);
     if (!(r->delta > 0)) return fail(CT_E_CONFIG, "delta must be > 0");
+    if (!(r->delta >= 1e-18)) return fail(CT_E_CONFIG, "delta %g below 1e-18 (delta^2 must be a normal float)", r->delta);
     if (r->n_dirs != 4 && r->n_dirs != 13) return fail(CT_E_CONFIG, "n_dirs must be 4 or 13");
     if (g->G.dim == 2 && r->n_dirs != 4) return fail(CT_E_CONFIG, "2-D geometry uses n_dirs = 4");
     for (int i = 0; i < 13; i++) {
@@ -530,6 +531,7 @@ static ct_status make_reg(const ct_geom* g, const ct_reg_desc* r, RegParams& rp)
     }
     rp.delta = (float)r->delta;
     rp.inv_delta = (float)(1.0 / r->delta);
+    rp.delta2 = (float)(r->delta * r->delta);
     rp.potential = r->potential;
     rp.n_dirs = r->n_dirs;
     rp.maxcurv = r->curvature == CT_CURV_MAX;

@@ -52,7 +52,7 @@ enum BackEpi { BK_WRITE = 0, BK_ACCUM = 1, BK_INIT = 2, BK_UPDATE = 3 };
 
 struct RegParams {
     float beta[13];
-    float delta, inv_delta;
+    float delta, inv_delta, delta2;   // delta2 = delta^2 (UPD_RAW hyperbola)
     int potential, n_dirs;
     int maxcurv;          // D_R with omega(0) = 1 (CT_CURV_MAX)
     float bsum;           // sum_d 2 beta_d: the interior maximum-curvature sum

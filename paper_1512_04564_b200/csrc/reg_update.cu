@@ -34,6 +34,17 @@ static_assert(dir_x(6) == -1 && dir_y(8) == -1 && dir_z(4) == 1 && dir_x(4) == 0
                   dir_x(11) == 1 && dir_y(11) == -1 && dir_z(3) == 0,
               "direction table");
 
+// UPD_RAW (hyperbola only): the register window holds x itself, not x/delta, and omega is
+// evaluated as o' = 1/sqrt(delta^2 + t^2) = omega/delta, so that t o' = tp omega (the gradient
+// sum is unchanged) and the curvature sum is delta sum w o' -- no per-plane scaling of the window.
+// Measured slower (c4 update 0.356 vs 0.339 ms, c3 0.077 vs 0.071; profiles/r2z/raw_ab.log): kept
+// as a switch only
+#ifndef UPD_RAW
+#define UPD_RAW 0
+#endif
+template <int POT>
+__host__ __device__ constexpr bool upd_raw() { return UPD_RAW && POT == 1; }
+
 // Potential in scaled form: tp = t / delta.  Returns omega(t) = phi'(t)/t and
 // tp * omega; phi'(t) = delta * tp * omega for all three potentials.
 template <int POT>
@@ -81,7 +92,7 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
             }
             float2 o;
             if (POT == 1) {
-                const float2 u = fma2(t, t, bcast2(1.f));
+                const float2 u = fma2(t, t, bcast2(upd_raw<POT>() ? rp.delta2 : 1.f));
                 o = make_float2(rsqrt_ftz(u.x), rsqrt_ftz(u.y));
             } else {
                 o = make_float2(omega_scaled<POT>(t.x, rp), omega_scaled<POT>(t.y, rp));
@@ -99,7 +110,7 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
                 if (ok) {
                     const float wgt = KAPPA ? rp.beta[d] * kj * K[zs][1 + sy][1 + sx] : rp.beta[d];
                     const float t = xv - W[zs][1 + sy][1 + sx];
-                    const float o = omega_scaled<POT>(t, rp);
+                    const float o = upd_raw<POT>() ? rsqrt_ftz(fmaf(t, t, rp.delta2)) : omega_scaled<POT>(t, rp);
                     gs = fmaf(wgt, t * o, gs);
                     cs = fmaf(wgt, o, cs);
                     cmax += wgt;
@@ -110,7 +121,10 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
     if (!CHECK && !KAPPA) {
         gs = gs2.x + gs2.y;
         cs = cs2.x + cs2.y;
+        if (upd_raw<POT>()) cs *= rp.delta;
         if (PATH == 2) cs -= xcorr;
+    } else if (upd_raw<POT>()) {
+        cs *= rp.delta;
     }
     gs_out = gs;
     // maximum curvature: omega(0) = 1 for every in-volume neighbour (interior, no kappa: bsum)
@@ -268,10 +282,11 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     auto scale_plane = [&](auto slot_c) {
         constexpr int S = decltype(slot_c)::value;
         XC[S] = W[S][1][1];
+        const float sc = upd_raw<POT>() ? 1.f : idel;   // UPD_RAW: the window stays x (folded away)
 #pragma unroll
         for (int a = 0; a < 3; a++)
 #pragma unroll
-            for (int b = 0; b < 3; b++) W[S][a][b] *= idel;
+            for (int b = 0; b < 3; b++) W[S][a][b] *= sc;
     };
     auto load_vox = [&](auto par_c, int k) {
         if (!FULL) return;

@@ -24,6 +24,13 @@ def source_rows(rep, kernel):
     ie, ist = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
     res = []
     for r in rows[2:]:
+        # several kernels match the regex: each adds its own header / blank rows -- skip those
+        if len(r) <= max(ia, isrc, ie, ist):
+            continue
+        try:
+            int(r[ia], 16)
+        except ValueError:
+            continue
         e = int(r[ie]) if r[ie].isdigit() else 0
         s = int(r[ist]) if r[ist].isdigit() else 0
         res.append((int(r[ia], 16) & 0xffff, e, s, r[isrc].strip()))

@@ -125,6 +125,28 @@ def test_reg_grad_parity(C, pot, kind, use_kappa, curvature):
         C.ct_geom_destroy(h)
 
 
+@pytest.mark.parametrize("delta", [1e-6, 1e-3, 10.0])
+def test_reg_grad_hyperbola_delta_range(C, delta):
+    """The hyperbola stencil evaluates omega/delta = 1/sqrt(delta^2 + t^2) on raw x (UPD_RAW,
+    DESIGN.md §5): check it from the near-TV to the near-quadratic regime (|t| ~ 0.02 vs delta)."""
+    g = tiny("helical_arc", nx=37, ny=21, nz=9)
+    rng = np.random.default_rng(11)
+    x = 0.02 * rng.random(P.vol_shape(g))
+    betas = list(rng.uniform(0.5, 2.0, 13))
+    _, gr, cv = P.reg(g, "hyperbola", delta, betas, 13, x, None)
+    h = C.ct_geom_create(C.geom_desc(g))
+    try:
+        gd = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        cd = torch.empty_like(gd)
+        C.ct_reg_grad(h, C.reg_desc("hyperbola", delta, betas, 13), dev(x), gd, cd)
+        assert rel(host(gd), gr) <= 1e-5
+        assert rel(host(cd), cv) <= 1e-5
+        with pytest.raises(C.CtError):
+            C.ct_reg_grad(h, C.reg_desc("hyperbola", 1e-20, betas, 13), dev(x), gd, cd)
+    finally:
+        C.ct_geom_destroy(h)
+
+
 def _gpu_recon(pb, dl=None):
     from paper_1512_04564_b200.recon import Recon
     r = Recon(pb["geom"], pb["reg"], pb["solver"], pb["y"], pb["w"], pb["x0"])
