@@ -195,6 +195,9 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 #ifndef UPD_ZDIV
 #define UPD_ZDIV 24
 #endif
+#ifndef UPD_CPA
+#define UPD_CPA 0   // D_L, g, htilde through a cp.async shared-memory ring 3 voxels ahead (FULL mode)
+#endif
 #ifndef UPD_MINB
 #define UPD_MINB 3  // <= 80 registers: 3 blocks of 256 per SM
 #endif
@@ -296,6 +299,26 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         Gv[Q] = __ldg(A.g + idx);
         Hv[Q] = A.ht[idx];
     };
+    // UPD_CPA: D_L, g, htilde of voxel k + 3 are copied into a per-thread shared-memory ring slot
+    // (k mod 4) by cp.async three steps ahead of their use (no registers held in flight)
+    constexpr bool CPA = FULL && UPD_CPA;
+    constexpr int nthr = 256;   // ring stride (>= threads per block)
+    float* ring = upd_sm + (A.pfx ? (size_t)blockDim.z * G.nz * 33 + (size_t)blockDim.z * NZC * 32 : 0) +
+                  ((jj * NZC + c) * 32 + lane);
+    auto issue_vox = [&](int k) {
+        if (!CPA) return;
+        if (act && k < k1) {
+            const unsigned idx = (unsigned)k * nxy + col;
+            float* r = ring + ((k & 3) * 3) * nthr;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(r)),
+                         "l"(__cvta_generic_to_global(A.dl + idx)) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(r + nthr)),
+                         "l"(__cvta_generic_to_global(A.g + idx)) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(r + 2 * nthr)),
+                         "l"(__cvta_generic_to_global(A.ht + idx)) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");   // one group per voxel, empty past the chunk
+    };
     float run = 0.f;
     // voxel k: planes k-1, k, k+1 in slots ZA, ZB, ZC (ZC loaded raw one step
     // ago: scaled now); plane k+2 is fetched into ZD and D_L, g, htilde of
@@ -305,7 +328,8 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         constexpr int Q = ZB & 1;
         scale_plane(zc);
         load_plane(zd, k + 2);
-        load_vox(std::integral_constant<int, Q ^ 1>(), k + 1);
+        if (CPA) issue_vox(k + 3);
+        else load_vox(std::integral_constant<int, Q ^ 1>(), k + 1);
         float xnew = 0.f;
         if (act) {
             const unsigned idx = (unsigned)k * nxy + col;
@@ -320,8 +344,19 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 1>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
             if (FULL) {
                 const float xv = XC[ZB];
-                const float d = Dv[Q], htv = Hv[Q];
-                const float s = fmaf(rho, htv, (1.f - rho) * Gv[Q]);
+                float d, htv, gv;
+                if (CPA) {
+                    asm volatile("cp.async.wait_group 3;" ::: "memory");   // voxel k's group (k+1..k+3 may pend)
+                    const float* r = ring + ((k & 3) * 3) * nthr;
+                    d = r[0];
+                    gv = r[nthr];
+                    htv = r[2 * nthr];
+                } else {
+                    d = Dv[Q];
+                    gv = Gv[Q];
+                    htv = Hv[Q];
+                }
+                const float s = fmaf(rho, htv, (1.f - rho) * gv);
                 const float den = fmaf(rho, d, 2.f * cs);
                 xnew = xv;
                 if (den > 0.f) xnew = fminf(fmaxf(xv - fmaf(del, gs, s) * rcp_ftz(den), A.box_lo), A.box_hi);
@@ -345,7 +380,13 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
     load_plane(I0(), k0 - 1);
     load_plane(I1(), k0);
     load_plane(I2(), k0 + 1);
-    load_vox(I1(), k0);
+    if (CPA) {
+        issue_vox(k0);
+        issue_vox(k0 + 1);
+        issue_vox(k0 + 2);
+    } else {
+        load_vox(I1(), k0);
+    }
     scale_plane(I0());
     scale_plane(I1());
     for (int k = k0; k < k1; k += 4) {
@@ -413,7 +454,7 @@ struct UpdShape {
     int nzc, cz, jpb;
     size_t smem;
 };
-static UpdShape upd_shape(const DGeom& G, bool pfx) {
+static UpdShape upd_shape(const DGeom& G, bool pfx, bool ring = false) {
     UpdShape u;
     constexpr int zdiv = UPD_ZDIV;   // voxels per z-chunk target (tuning variants: -DUPD_ZDIV=n)
     u.nzc = std::min(8, std::max(1, G.nz / std::max(1, zdiv)));
@@ -424,12 +465,13 @@ static UpdShape upd_shape(const DGeom& G, bool pfx) {
     u.nzc = (G.nz + u.cz - 1) / u.cz;
     u.jpb = std::max(1, 8 / u.nzc);  // JPB rows per block share x rows in L1
     u.smem = pfx ? sizeof(float) * ((size_t)u.jpb * G.nz * 33 + (size_t)u.jpb * u.nzc * 32) : 0;
+    if (ring) u.smem += sizeof(float) * 4 * 3 * 256;   // UPD_CPA ring: [slot][D_L, g, htilde][256 threads]
     return u;
 }
 
 template <int POT, int NDIRS, bool KAPPA, int MODE>
 static void upd_launch(const DGeom& G, const RegParams& rp, const Ctl* ctl, UpdArgs A, cudaStream_t s) {
-    const UpdShape u = upd_shape(G, A.pfx != nullptr);
+    const UpdShape u = upd_shape(G, A.pfx != nullptr, MODE == UPD_FULL && UPD_CPA);
     A.CZ = u.cz;
     dim3 block(32, u.nzc, u.jpb), grid((G.nx + 31) / 32, (G.ny + u.jpb - 1) / u.jpb, 1);
     if (u.smem > 48 * 1024)

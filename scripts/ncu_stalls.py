@@ -34,7 +34,7 @@ def source_rows(rep, kernel):
         e = int(r[ie]) if r[ie].isdigit() else 0
         s = int(r[ist]) if r[ist].isdigit() else 0
         res.append((int(r[ia], 16) & 0xffff, e, s, r[isrc].strip()))
-    return res
+    return list(dict.fromkeys(res))   # a kernel listed twice on the page: count each row once
 
 
 def main():
