@@ -196,7 +196,8 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 #define UPD_ZDIV 24
 #endif
 #ifndef UPD_CPA
-#define UPD_CPA 0   // D_L, g, htilde through a cp.async shared-memory ring 3 voxels ahead (FULL mode)
+#define UPD_CPA 0   // D_L, g, htilde through a cp.async shared-memory ring 3 voxels ahead (FULL mode);
+                    // measured no faster (c4 0.341 vs 0.339 ms, profiles/r2z/cpa_ab.log): a switch only
 #endif
 #ifndef UPD_MINB
 #define UPD_MINB 3  // <= 80 registers: 3 blocks of 256 per SM
