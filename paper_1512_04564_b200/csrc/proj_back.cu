@@ -99,6 +99,22 @@ k_back2(DGeom G, const float4* __restrict__ vtab, const Ctl* __restrict__ ctl, V
 #define BK_WMAX 6      // widest register window of detector columns (wider footprints: general loop)
 #endif
 
+// BK_PEEL: the row loop prefetches row o + 1 unconditionally and the last row is peeled (no
+// per-row select of the prefetch address: 62 instead of 67 instructions per 4 rows at W = 4).
+// Measured slower (c4 back 2.386 vs 2.247 ms, c3 0.298 vs 0.272, c5 14.10 vs 12.98;
+// profiles/r2fb/peel_ab.log): a switch only.
+#ifndef BK_PEEL
+#define BK_PEEL 0
+#endif
+// BK_PF2 = u > 0: the row loop requests row o + 2 while row o is summed (unrolled by u).
+#ifndef BK_PF2
+#define BK_PF2 0
+#endif
+// BK_RU: unroll factor of the row loop (4 = what the compiler picks on its own: the loads of four
+// rows are issued together).
+#ifndef BK_RU
+#define BK_RU 4
+#endif
 template <bool ARC, bool LZ, int W>
 __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WMAX], const float* __restrict__ pr,
                                           int sw, int tw, int n, float2* __restrict__ cs, float& run) {
@@ -106,10 +122,7 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
     float ofs = 0.5f;   // 1/2 - o
 #pragma unroll
     for (int q = 0; q < W; q++) a[q] = __ldg(pr + q);
-    for (int o = 0; o < n; o++) {
-        const float* __restrict__ pn = pr + (o + 1 < n ? G.ns : 0);
-#pragma unroll
-        for (int q = 0; q < W; q++) b[q] = __ldg(pn + q);
+    auto row = [&](int o) {
         float rs = 0.f;
 #pragma unroll
         for (int q = 0; q < W; q++) {
@@ -120,10 +133,54 @@ __device__ __forceinline__ void back_rows(const DGeom& G, const float (&F)[BK_WM
         cs[o * BK_BS] = make_float2(fmaf(ofs, rs, run), rs);
         run += rs;
         ofs -= 1.f;
+    };
+#if BK_PF2
+    // two rows ahead: row o + 2 is requested while row o is summed (c -> b -> a)
+    float c[W];
+    const int ns = G.ns;
+    {
+        const float* __restrict__ p1 = pr + (1 < n ? ns : 0);
+#pragma unroll
+        for (int q = 0; q < W; q++) b[q] = __ldg(p1 + q);
+        pr = p1;
+    }
+    constexpr int PFU = BK_PF2;
+#pragma unroll PFU
+    for (int o = 0; o < n; o++) {
+        const float* __restrict__ pn = pr + (o + 2 < n ? ns : 0);
+#pragma unroll
+        for (int q = 0; q < W; q++) c[q] = __ldg(pn + q);
+        row(o);
+        pr = pn;
+#pragma unroll
+        for (int q = 0; q < W; q++) {
+            a[q] = b[q];
+            b[q] = c[q];
+        }
+    }
+#elif BK_PEEL
+    for (int o = 0; o < n - 1; o++) {
+        pr += G.ns;
+#pragma unroll
+        for (int q = 0; q < W; q++) b[q] = __ldg(pr + q);
+        row(o);
+#pragma unroll
+        for (int q = 0; q < W; q++) a[q] = b[q];
+    }
+    row(n - 1);
+#else
+    constexpr int RU = BK_RU;
+#pragma unroll RU
+    for (int o = 0; o < n; o++) {
+        const float* __restrict__ pn = pr + (o + 1 < n ? G.ns : 0);
+#pragma unroll
+        for (int q = 0; q < W; q++) b[q] = __ldg(pn + q);
+        row(o);
         pr = pn;
 #pragma unroll
         for (int q = 0; q < W; q++) a[q] = b[q];
     }
+#endif
 }
 
 // ---------------------------------------------------------------------------
